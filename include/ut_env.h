@@ -1,0 +1,204 @@
+/* ut_env.h -- C-ABI drop-in boundary for the batched JaxLrauv environment step
+ * (arXiv 2505.08222) on B200 (sm_100a).
+ *
+ * Every entry point replaces one reference interface of the CPU library `utrack`
+ * (paths relative to /root/reference/proj/core). Plain C types only: no torch, no
+ * Eigen, no C++ exceptions cross this boundary. Status codes follow the reference's
+ * exception -> CLI exit-code mapping (tools/utrack.cpp:384-393):
+ *   ContractViolation -> 1, ConfigError -> 2, DataError -> 3 (errors.hpp:10-26);
+ * 4 is added for CUDA/runtime failures. The message of the last failure on the
+ * calling thread is available from ut_last_error().
+ *
+ * Threading/ownership (vecenv.hpp:18-23): a ut_vecenv is not reentrant; it owns
+ * every device buffer; pointers returned by ut_vecenv_buffers() stay valid until
+ * ut_vecenv_destroy(). Calls are synchronous: results are readable on return.
+ */
+#ifndef UT_ENV_H_
+#define UT_ENV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UT_ABI_VERSION 1
+
+enum ut_status {
+  UT_OK = 0,
+  UT_ERR_CONTRACT = 1, /* ContractViolation (errors.hpp:23-26) */
+  UT_ERR_CONFIG = 2,   /* ConfigError (errors.hpp:10-14) */
+  UT_ERR_DATA = 3,     /* DataError (errors.hpp:17-21) */
+  UT_ERR_RUNTIME = 4   /* CUDA / allocation failure (no reference counterpart) */
+};
+
+enum { UT_NUM_ACTIONS = 5, UT_FEATURE_DIM = 12 }; /* env_config.hpp:8, :13 */
+enum { UT_REWARD_TRACKING = 0, UT_REWARD_FOLLOW = 1 }; /* env_config.hpp:34 */
+enum { UT_POLICY_RANDOM = 0, UT_POLICY_SCRIPTED = 1 }; /* vecenv.hpp:16 */
+enum { UT_HEADING_DEFAULT = 0, UT_HEADING_BUCKET = 1 };
+
+/* PfConfig (env_config.hpp:36-42). */
+typedef struct ut_pf_config {
+  int32_t n_particles;       /* 1024 */
+  int32_t _pad0;
+  double process_noise_pos;  /* 1.0 m per step */
+  double process_noise_vel;  /* 0.05 m/s per step */
+  double speed_margin;       /* 1.2 */
+  double init_radius;        /* 450 m */
+} ut_pf_config;
+
+/* EnvConfig (env_config.hpp:44-93) as a POD. The heading model
+ * (kinematics.hpp:34-54) is carried as its resolved bucket for (agent_speed, dt):
+ * kind UT_HEADING_DEFAULT resolves it from the shipped default fit
+ * (kinematics.cpp:180-186) in ut_config_finalize(); UT_HEADING_BUCKET uses
+ * heading_a / heading_b as given. */
+typedef struct ut_env_config {
+  int32_t n_agents, n_targets, horizon, reward_mode;
+  double dt;
+  double agent_speed, target_speed_frac, target_speed_frac_max, target_turn_interval;
+  double detection_range, comm_range, comm_drop_prob, range_noise_std;
+  double eps_min, eps_max, d_min, d_safe;
+  double spawn_min_sep, spawn_max_sep, perturbation_std;
+  double target_depth_min, target_depth_max;
+  int32_t lost_steps;
+  int32_t heading_model_kind;
+  double heading_a, heading_b, heading_noise_std;
+  ut_pf_config pf;
+  /* Resolved by ut_config_finalize(): |heading_delta(0.24)| (env.cpp:115-116). */
+  double max_turn_per_step;
+} ut_env_config;
+
+/* Device views of the batch buffers (vecenv.hpp:51-62). Matrices are
+ * column-major like Eigen::MatrixXd: element (row, col) at ptr[col * rows + row].
+ *   obs / final_obs : rows ((env * n_agents + agent) * n_rows + row), 12 cols
+ *   global_state    : rows (env * n_rows + row), 12 cols
+ *   masks           : (env * n_agents + agent) * 5 + action
+ *   per-target info : env * n_targets + target                               */
+typedef struct ut_buffers {
+  int64_t n_envs;
+  int32_t n_agents, n_targets, n_rows, n_particles;
+  int64_t obs_rows, global_rows;
+  double* obs;
+  double* final_obs;
+  double* global_state;
+  double* rewards;
+  uint8_t* dones;
+  uint8_t* masks;
+  double* tracking_error;  /* StepOutput::tracking_error (env.hpp:57) */
+  double* min_agent_dist;  /* StepOutput::min_agent_dist (env.hpp:58) */
+  uint8_t* target_lost;    /* StepOutput::target_lost (env.hpp:59) */
+  uint8_t* collision;      /* StepOutput::collision (env.hpp:56) */
+  int32_t* step;           /* WorldState::step per env (env.hpp:50) */
+  int32_t* actions;        /* device action staging, n_envs * n_agents */
+  /* particle store, structure-of-arrays: field[set * n_particles + k],
+   * set = env * n_agents * n_targets + agent * n_targets + target */
+  double *px, *py, *vx, *vy, *w;
+} ut_buffers;
+
+/* Host destinations for ut_vecenv_copy_outputs(); NULL members are skipped. */
+typedef struct ut_host_outputs {
+  double* obs;
+  double* final_obs;
+  double* global_state;
+  double* rewards;
+  uint8_t* dones;
+  uint8_t* masks;
+  double* tracking_error;
+  double* min_agent_dist;
+  uint8_t* target_lost;
+  uint8_t* collision;
+  int32_t* step;
+} ut_host_outputs;
+
+/* Episode statistics accumulated on the device (marl.cpp:288-306 accumulators);
+ * the multi-GPU driver all-reduces this vector once per report interval. */
+enum {
+  UT_STAT_ENV_STEPS = 0,      /* env-steps taken                          */
+  UT_STAT_REWARD_SUM,         /* sum of step rewards                      */
+  UT_STAT_TRACK_ERR_SUM,      /* sum over env-steps of mean target error  */
+  UT_STAT_EPISODES_DONE,      /* completed episodes                       */
+  UT_STAT_EPISODE_RETURN_SUM, /* sum of completed-episode returns         */
+  UT_STAT_COLLISION_STEPS,    /* env-steps with a collision               */
+  UT_STAT_LOST_TARGET_STEPS,  /* (env, target)-steps flagged lost         */
+  UT_STAT_PF_UPDATES,         /* particle-filter measurement updates      */
+  UT_STAT_PF_RESAMPLES,       /* particle-filter resamples                */
+  UT_N_STATS
+};
+
+/* BenchmarkReport (vecenv.hpp:87-98), device-timed. */
+typedef struct ut_benchmark_report {
+  int64_t n_envs;
+  int32_t n_agents, n_targets, timed_steps, _pad0;
+  double wall_seconds; /* CUDA-event time of the timed steps */
+  double sps;          /* env-steps per second, n_envs * steps / seconds (vecenv.cpp:198) */
+  double agent_sps;    /* sps * n_agents */
+} ut_benchmark_report;
+
+typedef struct ut_vecenv ut_vecenv;
+
+/* ---- configuration ---------------------------------------------------- */
+/* EnvConfig{} defaults (env_config.hpp:44-80). */
+void ut_config_default(ut_env_config* cfg);
+/* EnvConfig::finalize (env.cpp:40-65): validates every field (UT_ERR_CONFIG naming
+ * the field) and resolves the heading bucket and max turn. */
+int ut_config_finalize(ut_env_config* cfg);
+
+/* ---- VecEnv ------------------------------------------------------------- */
+/* VecEnv::VecEnv (vecenv.cpp:7-45) = n_envs x Environment::Environment(cfg, seed, i)
+ * (env.cpp:110-151). Env i of this shard has GLOBAL index env_index_offset + i,
+ * which keys its RNG streams (env.cpp:113-114, 130-133), so a shard of a larger
+ * batch is bit-identical to the same envs of the unsharded batch. */
+int ut_vecenv_create(const ut_env_config* cfg, int64_t n_envs, uint64_t master_seed,
+                     int64_t env_index_offset, int device, ut_vecenv** out);
+/* Heterogeneous fleets (no reference counterpart: the reference VecEnv is
+ * homogeneous, vecenv.cpp:7-22): env i uses cfgs[cfg_of_env[i]]. Batch buffers are
+ * padded to the largest n_agents / n_rows / n_targets (padding rows are zero). */
+int ut_vecenv_create_mixed(const ut_env_config* cfgs, int32_t n_cfgs,
+                           const int32_t* cfg_of_env, int64_t n_envs, uint64_t master_seed,
+                           int64_t env_index_offset, int device, ut_vecenv** out);
+void ut_vecenv_destroy(ut_vecenv* v);
+
+/* VecEnv::reset_all (vecenv.cpp:69-77). */
+int ut_vecenv_reset_all(ut_vecenv* v);
+/* VecEnv::step (vecenv.cpp:79-116): actions row-major n_envs x n_agents, host or
+ * device memory. Every action is validated BEFORE any env steps; on a violation
+ * nothing is mutated and UT_ERR_CONTRACT names the lowest failing env ("env i: ..."). */
+int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device);
+/* VecEnv::step_policy (vecenv.cpp:118-143), policy UT_POLICY_*. n_steps > 1 runs
+ * that many steps back to back (CUDA-graph replay, no host round trip). */
+int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps);
+/* VecEnv::refresh_outputs (vecenv.cpp:145-150). */
+int ut_vecenv_refresh_outputs(ut_vecenv* v);
+
+int ut_vecenv_buffers(ut_vecenv* v, ut_buffers* out);
+int ut_vecenv_copy_outputs(ut_vecenv* v, const ut_host_outputs* dst);
+/* Runs subsequent work on a caller-owned cudaStream_t (NULL = the handle's own). */
+int ut_vecenv_set_stream(ut_vecenv* v, void* cuda_stream);
+int ut_vecenv_synchronize(ut_vecenv* v);
+/* Reads (and optionally zeroes) the device statistics vector. */
+int ut_vecenv_stats(ut_vecenv* v, double out[UT_N_STATS], int reset);
+/* Number of kernels this handle has launched so far. */
+int64_t ut_vecenv_launch_count(const ut_vecenv* v);
+
+/* ---- per-env state (Environment API) ----------------------------------- */
+/* Environment::serialize_state / deserialize_state (env.cpp:550-659), identical
+ * blob layout: 5 + 6A + 9T + A*(6A + T*(9 + 5P)) doubles. `len` receives the
+ * required length; UT_ERR_DATA if `cap` is too small / the blob is malformed. */
+int ut_env_serialize(ut_vecenv* v, int64_t env, double* blob, size_t cap, size_t* len);
+int ut_env_deserialize(ut_vecenv* v, int64_t env, const double* blob, size_t len);
+/* world().step (env.hpp:50), read by Trainer::collect_rollout (marl.cpp:211,227). */
+int ut_env_world_step(ut_vecenv* v, int64_t env, int32_t* step);
+
+/* ---- benchmark ------------------------------------------------------------ */
+/* benchmark_sps (vecenv.cpp:175-202) on the device: warmup + timed step_policy. */
+int ut_benchmark_sps(const ut_env_config* cfg, int64_t n_envs, int32_t n_steps, int policy,
+                     uint64_t seed, int32_t warmup, int device, ut_benchmark_report* out);
+
+const char* ut_last_error(void);
+int ut_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UT_ENV_H_ */

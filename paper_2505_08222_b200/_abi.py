@@ -1,0 +1,133 @@
+"""ctypes mirror of include/ut_env.h (the C-ABI drop-in boundary).
+
+Field order and types must match the header exactly; tests/test_abi.py checks the
+sizes against the compiled library.
+"""
+import ctypes as C
+
+UT_OK, UT_ERR_CONTRACT, UT_ERR_CONFIG, UT_ERR_DATA, UT_ERR_RUNTIME = 0, 1, 2, 3, 4
+UT_NUM_ACTIONS = 5
+UT_FEATURE_DIM = 12
+UT_REWARD_TRACKING, UT_REWARD_FOLLOW = 0, 1
+UT_POLICY_RANDOM, UT_POLICY_SCRIPTED = 0, 1
+UT_HEADING_DEFAULT, UT_HEADING_BUCKET = 0, 1
+
+STAT_NAMES = (
+    "env_steps", "reward_sum", "track_err_sum", "episodes_done", "episode_return_sum",
+    "collision_steps", "lost_target_steps", "pf_updates", "pf_resamples",
+)
+UT_N_STATS = len(STAT_NAMES)
+
+
+class PfConfig(C.Structure):
+    """PfConfig (env_config.hpp:36-42)."""
+    _fields_ = [
+        ("n_particles", C.c_int32), ("_pad0", C.c_int32),
+        ("process_noise_pos", C.c_double), ("process_noise_vel", C.c_double),
+        ("speed_margin", C.c_double), ("init_radius", C.c_double),
+    ]
+
+
+class EnvConfigC(C.Structure):
+    """EnvConfig (env_config.hpp:44-93) as the ABI POD."""
+    _fields_ = [
+        ("n_agents", C.c_int32), ("n_targets", C.c_int32), ("horizon", C.c_int32),
+        ("reward_mode", C.c_int32),
+        ("dt", C.c_double),
+        ("agent_speed", C.c_double), ("target_speed_frac", C.c_double),
+        ("target_speed_frac_max", C.c_double), ("target_turn_interval", C.c_double),
+        ("detection_range", C.c_double), ("comm_range", C.c_double),
+        ("comm_drop_prob", C.c_double), ("range_noise_std", C.c_double),
+        ("eps_min", C.c_double), ("eps_max", C.c_double), ("d_min", C.c_double),
+        ("d_safe", C.c_double),
+        ("spawn_min_sep", C.c_double), ("spawn_max_sep", C.c_double),
+        ("perturbation_std", C.c_double),
+        ("target_depth_min", C.c_double), ("target_depth_max", C.c_double),
+        ("lost_steps", C.c_int32), ("heading_model_kind", C.c_int32),
+        ("heading_a", C.c_double), ("heading_b", C.c_double), ("heading_noise_std", C.c_double),
+        ("pf", PfConfig),
+        ("max_turn_per_step", C.c_double),
+    ]
+
+
+class Buffers(C.Structure):
+    _fields_ = [
+        ("n_envs", C.c_int64),
+        ("n_agents", C.c_int32), ("n_targets", C.c_int32), ("n_rows", C.c_int32),
+        ("n_particles", C.c_int32),
+        ("obs_rows", C.c_int64), ("global_rows", C.c_int64),
+        ("obs", C.c_void_p), ("final_obs", C.c_void_p), ("global_state", C.c_void_p),
+        ("rewards", C.c_void_p), ("dones", C.c_void_p), ("masks", C.c_void_p),
+        ("tracking_error", C.c_void_p), ("min_agent_dist", C.c_void_p),
+        ("target_lost", C.c_void_p), ("collision", C.c_void_p), ("step", C.c_void_p),
+        ("actions", C.c_void_p),
+        ("px", C.c_void_p), ("py", C.c_void_p), ("vx", C.c_void_p), ("vy", C.c_void_p),
+        ("w", C.c_void_p),
+    ]
+
+
+class HostOutputs(C.Structure):
+    _fields_ = [
+        ("obs", C.c_void_p), ("final_obs", C.c_void_p), ("global_state", C.c_void_p),
+        ("rewards", C.c_void_p), ("dones", C.c_void_p), ("masks", C.c_void_p),
+        ("tracking_error", C.c_void_p), ("min_agent_dist", C.c_void_p),
+        ("target_lost", C.c_void_p), ("collision", C.c_void_p), ("step", C.c_void_p),
+    ]
+
+
+class BenchmarkReport(C.Structure):
+    _fields_ = [
+        ("n_envs", C.c_int64), ("n_agents", C.c_int32), ("n_targets", C.c_int32),
+        ("timed_steps", C.c_int32), ("_pad0", C.c_int32),
+        ("wall_seconds", C.c_double), ("sps", C.c_double), ("agent_sps", C.c_double),
+    ]
+
+
+HOST_OUTPUT_FIELDS = tuple(name for name, _ in HostOutputs._fields_)
+
+
+def declare_product(lib):
+    """Attach argtypes/restype for every entry point declared in ut_env.h."""
+    P, I32, I64, U64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64
+    cfgp = C.POINTER(EnvConfigC)
+    sig = {
+        "ut_config_default": (None, [cfgp]),
+        "ut_config_finalize": (C.c_int, [cfgp]),
+        "ut_vecenv_create": (C.c_int, [cfgp, I64, U64, I64, C.c_int, C.POINTER(P)]),
+        "ut_vecenv_create_mixed": (C.c_int, [cfgp, I32, C.POINTER(I32), I64, U64, I64, C.c_int,
+                                             C.POINTER(P)]),
+        "ut_vecenv_destroy": (None, [P]),
+        "ut_vecenv_reset_all": (C.c_int, [P]),
+        "ut_vecenv_step": (C.c_int, [P, P, C.c_int]),
+        "ut_vecenv_step_policy": (C.c_int, [P, C.c_int, C.c_int]),
+        "ut_vecenv_refresh_outputs": (C.c_int, [P]),
+        "ut_vecenv_buffers": (C.c_int, [P, C.POINTER(Buffers)]),
+        "ut_vecenv_copy_outputs": (C.c_int, [P, C.POINTER(HostOutputs)]),
+        "ut_vecenv_set_stream": (C.c_int, [P, P]),
+        "ut_vecenv_synchronize": (C.c_int, [P]),
+        "ut_vecenv_stats": (C.c_int, [P, C.POINTER(C.c_double), C.c_int]),
+        "ut_vecenv_launch_count": (I64, [P]),
+        "ut_env_serialize": (C.c_int, [P, I64, C.POINTER(C.c_double), C.c_size_t,
+                                       C.POINTER(C.c_size_t)]),
+        "ut_env_deserialize": (C.c_int, [P, I64, C.POINTER(C.c_double), C.c_size_t]),
+        "ut_env_world_step": (C.c_int, [P, I64, C.POINTER(I32)]),
+        "ut_benchmark_sps": (C.c_int, [cfgp, I64, I32, C.c_int, U64, I32, C.c_int,
+                                       C.POINTER(BenchmarkReport)]),
+        "ut_last_error": (C.c_char_p, []),
+        "ut_abi_version": (C.c_int, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+PRODUCT_SYMBOLS = (
+    "ut_config_default", "ut_config_finalize", "ut_vecenv_create", "ut_vecenv_create_mixed",
+    "ut_vecenv_destroy", "ut_vecenv_reset_all", "ut_vecenv_step", "ut_vecenv_step_policy",
+    "ut_vecenv_refresh_outputs", "ut_vecenv_buffers", "ut_vecenv_copy_outputs",
+    "ut_vecenv_set_stream", "ut_vecenv_synchronize", "ut_vecenv_stats", "ut_vecenv_launch_count",
+    "ut_env_serialize", "ut_env_deserialize", "ut_env_world_step", "ut_benchmark_sps",
+    "ut_last_error", "ut_abi_version",
+)
