@@ -1,0 +1,341 @@
+#!/usr/bin/env python3
+"""Throughput of the batched JaxLrauv environment step on B200.
+
+Metric (BASELINE.json): agent-env steps/sec on the 5-agent / 5-fast-target
+workload (65,536 envs per GPU, P = 1024, fp64 particle
+filters), random legal actions from the device bench stream (vecenv.cpp:118-135).
+Multi-GPU (torchrun): envs shard by global index range, each GPU steps its
+shard independently (weak scaling, no data-path collective); the episode
+statistics are all-reduced once over NCCL after the run.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+"""
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # SURVEY §8d synthetic inputs; everything else takes the EnvConfig defaults
+    "c1": dict(desc="1 agent vs 1 slow target", n_agents=1, n_targets=1, target_speed_frac=0.3,
+               horizon=128, envs=1024),
+    "c2": dict(desc="2 agents vs 2 targets, 1000-step episodes", n_agents=2, n_targets=2, horizon=1000,
+               envs=16384),
+    "c3": dict(desc="5 agents vs 5 fast targets (paper headline)", n_agents=5, n_targets=5,
+               target_speed_frac=0.6, d_min=100.0, spawn_max_sep=400.0, horizon=128, envs=65536),
+    "c5": dict(desc="5v5 estimator-heavy (every pair pinged, every link up)", n_agents=5, n_targets=5,
+               target_speed_frac=0.6, d_min=100.0, spawn_max_sep=400.0, horizon=128,
+               comm_drop_prob=0.0, detection_range=1e9, comm_range=1e9, envs=131072),
+}
+
+
+def make_cfg(name, particles=1024):
+    from paper_2505_08222_b200.vecenv import EnvConfig, PfConfig
+    kw = {k: v for k, v in CONFIGS[name].items() if k not in ("desc", "envs")}
+    return EnvConfig(**kw, pf=PfConfig(n_particles=particles))
+
+
+def oracle_cfg(name, particles=1024):
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_bindings import default_config
+    kw = {k: v for k, v in CONFIGS[name].items() if k not in ("desc", "envs")}
+    return default_config(**kw, pf_n_particles=particles)
+
+
+def algorithmic_bytes_per_env_step(A, T, P, rec_words):
+    """read + write of the whole state once per step (80 B per
+    particle), the env record (read + write), and the step's outputs."""
+    R = A + T
+    pf = 80 * P * A * T
+    rec = 16 * rec_words
+    outs = 8 * 12 * A * R + 8 * 12 * R + 8 + 1 + 5 * A + T * (8 + 8 + 1) + 1 + 4
+    return pf + rec + outs
+
+
+def rec_words_for(A, T):
+    o_track = 8 + 6 * A + 8 * T + T + 6 * A * A
+    o_stats = o_track + 9 * A * T
+    return (o_stats + 9 + 1) & ~1
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = pathlib.Path(f"/tmp/ut_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.gpu)], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def cpu_baseline(cfg_name, particles, budget_s=12.0):
+    """The reference's own benchmark_sps (vecenv.cpp:175-202), compiled from its
+    sources into oracle/_ref, on this host's cores over a bounded sample."""
+    import ctypes as C
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracle_bindings as ob
+    cfg = oracle_cfg(cfg_name, particles)
+    cores = ob.env_cpu_count()
+    A = CONFIGS[cfg_name]["n_agents"]
+    n_envs = max(32 * cores, 64)
+    if ob.ref_available():
+        lib = ob.ref_lib()
+        kind = "reference"
+
+        def run(steps, warm):
+            sps, wall, wk, tot = C.c_double(), C.c_double(), C.c_int32(), C.c_uint64()
+            ph = (C.c_uint64 * 7)()
+            rc = lib.ref_benchmark_sps(C.byref(cfg), n_envs, steps, 0, 0, cores, warm, C.byref(sps), C.byref(wall),
+                                       C.byref(wk), ph, C.byref(tot))
+            if rc:
+                raise RuntimeError(lib.ref_last_error().decode())
+            return sps.value, wall.value, wk.value, list(ph)
+    else:
+        kind = "port"
+        cores = 1
+        n_envs = 16
+
+        def run(steps, warm):
+            o = ob.Oracle(cfg, n_envs, 0)
+            o.step_policy(warm)
+            t0 = time.perf_counter()
+            o.step_policy(steps)
+            wall = time.perf_counter() - t0
+            o.close()
+            return n_envs * steps / wall, wall, 1, []
+    sps, wall, wk, ph = run(1, 1)  # probe
+    steps = int(max(2, min(64, budget_s / max(wall, 1e-3))))
+    sps, wall, wk, ph = run(steps, 2)
+    names = ["targets", "agents", "measure", "filter", "comms", "observe", "reward"]
+    return {"value": sps * A, "unit": "agent-env steps/s", "cores": wk, "kind": kind,
+            "sample": f"{n_envs} envs x {steps} steps of {cfg_name} (P={particles}), "
+                      f"benchmark_sps(kRandom) after 2 warmup steps, {wall:.1f} s wall",
+            "env_sps": sps, "phase_ns": dict(zip(names, ph)) if ph else None}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    base = cpu_baseline(args.config, args.particles, budget_s=max(5.0, 2.0 * (args.steps + args.warmup)))
+    line = {
+        "metric": "agent-env steps/sec (5v5 fast targets)" if args.config == "c3" else f"agent-env steps/sec ({args.config})",
+        "value": base["value"], "unit": "agent-env steps/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}", "particles": args.particles},
+        "cpu_baseline": base,
+        "e2e": {"value": base["value"], "unit": "agent-env steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--envs-per-gpu", type=int, default=None)
+    ap.add_argument("--particles", type=int, default=1024)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic-bytes", type=float, default=None,
+                    help="dram bytes per launch from an ncu --set full capture (profiles/)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2505_08222_b200.vecenv import VecEnv
+    from paper_2505_08222_b200.sharding import shard_range
+
+    cfg = make_cfg(args.config, args.particles)
+    A, T, P = cfg.n_agents, cfg.n_targets, cfg.pf.n_particles
+    per_gpu = args.envs_per_gpu or CONFIGS[args.config]["envs"]
+    total = per_gpu * world
+    lo, hi = shard_range(total, rank, world)
+    venv = VecEnv(cfg, hi - lo, master_seed=0, env_index_offset=lo, device=local)
+    stream = torch.cuda.current_stream()
+    venv.set_stream(stream.cuda_stream)
+
+    venv.step_policy("random", args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = venv.launch_count()
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record(stream)
+        venv.step_policy("random", args.steps)
+        end.record(stream)
+        torch.cuda.synchronize()
+    gpu_launches = venv.launch_count() - launches0
+    ms = start.elapsed_time(end)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    secs = ms_max / 1e3
+    env_steps = total * args.steps
+    value = env_steps * A / secs
+
+    # episode statistics: the one NCCL collective (north_star)
+    st = torch.tensor(venv.stats(), dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(st)
+    st = st.cpu().numpy()
+
+    # ---- e2e through the public API with host buffers (pinned), copies timed
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 10)
+    n_loc = hi - lo
+    acts_h = torch.empty((n_loc, A), dtype=torch.int32, pin_memory=True)
+    host = {
+        "obs": torch.empty((12, n_loc * A * (A + T)), dtype=torch.float64, pin_memory=True),
+        "global_state": torch.empty((12, n_loc * (A + T)), dtype=torch.float64, pin_memory=True),
+        "rewards": torch.empty(n_loc, dtype=torch.float64, pin_memory=True),
+        "dones": torch.empty(n_loc, dtype=torch.uint8, pin_memory=True),
+        "masks": torch.empty(n_loc * A * 5, dtype=torch.uint8, pin_memory=True),
+        "tracking_error": torch.empty(n_loc * T, dtype=torch.float64, pin_memory=True),
+        "min_agent_dist": torch.empty(n_loc * T, dtype=torch.float64, pin_memory=True),
+        "target_lost": torch.empty(n_loc * T, dtype=torch.uint8, pin_memory=True),
+        "collision": torch.empty(n_loc, dtype=torch.uint8, pin_memory=True),
+    }
+    d2h = sum(v.numel() * v.element_size() for v in host.values())
+    h2d = acts_h.numel() * 4
+    venv.copy_outputs_into({"masks": host["masks"]})
+    rng = np.random.default_rng(rank)
+    acts_np = acts_h.numpy()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        # host policy: uniform legal action from the returned masks
+        cs = np.cumsum(host["masks"].numpy().reshape(n_loc, A, 5), axis=2)
+        k = (rng.random((n_loc, A)) * cs[:, :, -1]).astype(np.int64)
+        acts_np[:] = np.argmax(cs > k[:, :, None], axis=2)
+        venv.step(acts_np)
+        venv.copy_outputs_into(host)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = total * e2e_steps * A / float(te.item())
+
+    peak, peak_kind = measured_peaks()
+    bytes_launch = algorithmic_bytes_per_env_step(A, T, P, rec_words_for(A, T)) * (hi - lo)
+    avg_launch_s = secs / max(1, args.steps)
+    achieved = bytes_launch / avg_launch_s / 1e9
+
+    line = {
+        "metric": "agent-env steps/sec (5v5 fast targets)" if args.config == "c3" else f"agent-env steps/sec ({args.config})",
+        "value": value, "unit": "agent-env steps/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}", "envs_per_gpu": per_gpu,
+                   "total_envs": total, "particles": P, "agents": A, "targets": T,
+                   "policy": "device random legal (bench stream, vecenv.cpp:125-134)",
+                   "l2": f"inputs larger than L2 ({bytes_launch / 1e9:.1f} GB touched per step per GPU)",
+                   "env_steps_per_s": env_steps / secs},
+        "e2e": {"value": e2e_value, "unit": "agent-env steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "path": "VecEnv.step(host int32 actions) + copy_outputs to pinned host (ut_vecenv_step + ut_vecenv_copy_outputs)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": args.traffic_bytes,
+                     "kernel": "step_kernel<4>", "bytes_per_launch": bytes_launch,
+                     "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_kind},
+        "gpu_launches": gpu_launches,
+        "clocks": clocks.summary(),
+        "stats": {k: float(v) for k, v in zip(
+            ("env_steps", "reward_sum", "track_err_sum", "episodes_done", "episode_return_sum",
+             "collision_steps", "lost_target_steps", "pf_updates", "pf_resamples"), st)},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.config, P)
+        except Exception as exc:  # noqa: BLE001 -- reported, not fatal
+            line["cpu_baseline"] = {"value": None, "error": str(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    venv.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,24 @@
+/* ut_debug.h -- verification entry points of libutrack_b200.so (not part of the
+ * reference-facing boundary). Used by the GPU parity tests to check the device
+ * primitives exhaustively against the oracle. */
+#ifndef UT_DEBUG_H_
+#define UT_DEBUG_H_
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* Evaluates the device's fp32 noise transcendental on its whole 2^24-point input
+ * grid (tracking.cpp:29-36): kind 0 = log(((i)+1) * 2^-24), 1 = cos(2pi_f * i*2^-24),
+ * 2 = sin(2pi_f * i*2^-24). host_out receives 2^24 floats. */
+int ut_debug_cr_grid(int kind, int device, float* host_out);
+/* n consecutive Philox4x32-10 blocks from block0 (rng.hpp:116-131): 4n words. */
+int ut_debug_philox(uint64_t key, uint64_t stream, uint64_t block0, int32_t n, int device, uint32_t* host_out);
+/* sizeof of the ABI structs as compiled: ut_env_config, ut_buffers,
+ * ut_host_outputs, ut_benchmark_report (no device needed). */
+int ut_debug_abi_sizes(int64_t out[4]);
+/* derive_key (rng.hpp:30-38) evaluated on the device. */
+int ut_debug_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t d, int device, uint64_t* out);
+#ifdef __cplusplus
+}
+#endif
+#endif

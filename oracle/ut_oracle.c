@@ -162,6 +162,20 @@ float uto_cr_logf(float x) { return (float)log((double)x); }
 float uto_cr_cosf(float x) { return (float)cos((double)x); }
 float uto_cr_sinf(float x) { return (float)sin((double)x); }
 
+/* The whole 2^24-point input grid of one noise transcendental (tracking.cpp:29-36):
+ * kind 0: log(((i)+1) 2^-24); 1: cos(2pi_f i 2^-24); 2: sin(2pi_f i 2^-24). */
+void uto_cr_grid(int kind, float* out) {
+  const float two_pi_f = 2.0f * (float)UTO_PI;
+  for (uint32_t i = 0; i < (1u << 24); ++i) {
+    if (kind == 0) {
+      out[i] = uto_cr_logf((float)(i + 1u) * 0x1.0p-24f);
+    } else {
+      const float a = two_pi_f * ((float)i * 0x1.0p-24f);
+      out[i] = kind == 1 ? uto_cr_cosf(a) : uto_cr_sinf(a);
+    }
+  }
+}
+
 /* ---------------------------------------------------------- kinematics --- */
 /* kinematics.cpp:13-18 */
 static double wrap_angle(double psi) {

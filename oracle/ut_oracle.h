@@ -40,6 +40,7 @@ uint64_t uto_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t d);
 float uto_cr_logf(float x);
 float uto_cr_cosf(float x);
 float uto_cr_sinf(float x);
+void uto_cr_grid(int kind, float* out);
 /* fills out[0..4n) with the predict noise of one particle set starting at u32
  * stream position `pos` (tracking.cpp:24-37) */
 void uto_fill_normals(uint64_t key, uint64_t stream, uint64_t pos, int64_t n, float* out);

@@ -123,6 +123,19 @@ def declare_product(lib):
     return lib
 
 
+def declare_debug(lib):
+    """Signatures of include/ut_debug.h."""
+    lib.ut_debug_cr_grid.argtypes = [C.c_int, C.c_int, C.c_void_p]
+    lib.ut_debug_cr_grid.restype = C.c_int
+    lib.ut_debug_philox.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int, C.c_void_p]
+    lib.ut_debug_philox.restype = C.c_int
+    lib.ut_debug_derive_key.argtypes = [C.c_uint64] * 4 + [C.c_int, C.POINTER(C.c_uint64)]
+    lib.ut_debug_derive_key.restype = C.c_int
+    lib.ut_debug_abi_sizes.argtypes = [C.POINTER(C.c_int64)]
+    lib.ut_debug_abi_sizes.restype = C.c_int
+    return lib
+
+
 PRODUCT_SYMBOLS = (
     "ut_config_default", "ut_config_finalize", "ut_vecenv_create", "ut_vecenv_create_mixed",
     "ut_vecenv_destroy", "ut_vecenv_reset_all", "ut_vecenv_step", "ut_vecenv_step_policy",

@@ -1,0 +1,28 @@
+"""Loader for the in-tree CUDA library. There is no fallback: if the library is
+missing or cannot be loaded, every entry point raises."""
+import ctypes as C
+import pathlib
+
+from . import _abi
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libutrack_b200.so"
+_lib = None
+
+
+class NativeLibraryMissing(RuntimeError):
+    pass
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise NativeLibraryMissing(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2505_08222_b200.build` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        handle = C.CDLL(str(LIB_PATH))
+        _abi.declare_product(handle)
+        if handle.ut_abi_version() != 1:
+            raise NativeLibraryMissing("libutrack_b200.so ABI version mismatch")
+        _lib = handle
+    return _lib

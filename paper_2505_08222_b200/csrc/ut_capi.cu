@@ -1,0 +1,800 @@
+// ut_capi.cu -- host side of the C-ABI (include/ut_env.h): device memory, launch
+// configuration and the reference's VecEnv/Environment semantics around the
+// fused step kernel. No CPU fallback: every state transition runs on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ut_env.h"
+#include "ut_kernels.cuh"
+
+using namespace ut;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define UT_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t err_ = (call);                                                            \
+    if (err_ != cudaSuccess)                                                              \
+      return fail(UT_ERR_RUNTIME, "%s failed: %s", #call, cudaGetErrorString(err_));      \
+  } while (0)
+
+// ------------------------------------------------------------ config ---
+// Default heading bucket: OLS over the shipped synthetic calibration rows of
+// (speed, dt) (kinematics.cpp:58-111 fit, :131-154 synth, :119 oracle, :180-186).
+// Compiled with -ffp-contract=off like the oracle, so (a, b) are bit-identical.
+bool default_bucket(double speed, double dt, double* a_out, double* b_out) {
+  static const double speeds[] = {0.5, 0.75, 1.0, 1.25, 1.5, 2.0};
+  static const double dts[] = {10.0, 15.0, 30.0, 60.0};
+  if (std::find(std::begin(speeds), std::end(speeds), speed) == std::end(speeds)) return false;
+  if (std::find(std::begin(dts), std::end(dts), dt) == std::end(dts)) return false;
+  constexpr int kRows = 201;
+  constexpr double kMax = 0.24, kGain = 0.15;
+  double sx = 0.0, sy = 0.0, sxx = 0.0, sxy = 0.0;
+  for (int i = 0; i < kRows; ++i) {
+    const double t = static_cast<double>(i) / (kRows - 1);
+    const double gamma = -kMax + 2.0 * kMax * t;
+    const double dpsi = kGain * speed * dt * std::tan(gamma) + 0.0;
+    sx += gamma;
+    sy += dpsi;
+    sxx += gamma * gamma;
+    sxy += gamma * dpsi;
+  }
+  const double n = kRows;
+  const double denom = n * sxx - sx * sx;
+  *a_out = (n * sxy - sx * sy) / denom;
+  *b_out = (sy - *a_out * sx) / n;
+  return true;
+}
+
+DevConfig to_dev(const ut_env_config& c) {
+  DevConfig d{};
+  d.A = c.n_agents;
+  d.T = c.n_targets;
+  d.P = c.pf.n_particles;
+  d.horizon = c.horizon;
+  d.reward_mode = c.reward_mode;
+  d.lost_steps = c.lost_steps;
+  d.noise_on = (c.pf.process_noise_pos > 0.0 || c.pf.process_noise_vel > 0.0) ? 1 : 0;
+  d.dt = c.dt;
+  d.agent_speed = c.agent_speed;
+  d.tgt_lo = c.agent_speed * c.target_speed_frac;  // env_config.hpp:85-88
+  d.tgt_hi = c.agent_speed * std::max(c.target_speed_frac, c.target_speed_frac_max);
+  d.turn_interval = c.target_turn_interval;
+  d.det_range = c.detection_range;
+  d.comm_range = c.comm_range;
+  d.drop = c.comm_drop_prob;
+  d.range_noise = c.range_noise_std;
+  d.sigma_meas = std::max(c.range_noise_std, 0.1);  // env.cpp:340
+  d.eps_min = c.eps_min;
+  d.eps_max = c.eps_max;
+  d.d_min = c.d_min;
+  d.d_safe = c.d_safe;
+  d.min_sep = c.spawn_min_sep;
+  d.disc_r = c.spawn_max_sep / 2.0;
+  d.pert_std = c.perturbation_std;
+  d.depth_min = c.target_depth_min;
+  d.depth_max = c.target_depth_max;
+  d.pn = c.pf.process_noise_pos;
+  d.vn = c.pf.process_noise_vel;
+  d.speed_margin = c.pf.speed_margin;
+  d.init_radius = c.pf.init_radius;
+  d.head_a = c.heading_a;
+  d.head_b = c.heading_b;
+  d.head_noise = c.heading_noise_std;
+  d.max_turn = c.max_turn_per_step;
+  layout_config(d);
+  return d;
+}
+
+constexpr int kPPT = 4;
+constexpr int kMaxParticles = 4096;
+
+int threads_for(int P) {
+  int nt = (P + kPPT - 1) / kPPT;
+  nt = (nt + 31) / 32 * 32;
+  return std::max(32, nt);
+}
+
+struct DeviceBuf {
+  void* p = nullptr;
+  ~DeviceBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+struct ut_vecenv {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int64_t n_envs = 0;
+  int64_t offset = 0;
+  uint64_t seed = 0;
+  std::vector<ut_env_config> cfgs;
+  std::vector<DevConfig> dcfgs;
+  std::vector<int32_t> cfg_of_env;  // empty: homogeneous
+  std::vector<int64_t> rec_off, set_off;
+  int64_t total_sets = 0, total_rec = 0;
+  int A_max = 0, T_max = 0, R_max = 0, P = 0, rec_words_max = 0;
+  int nt = 0;
+  size_t smem = 0;
+  DevBatch B{};
+  std::vector<void*> allocs;
+  int32_t* d_status = nullptr;  // [0] status, [1] error_env
+  int32_t* h_status = nullptr;  // pinned
+  int64_t launches = 0;
+
+  ~ut_vecenv() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : allocs) cudaFree(p);
+    if (h_status) cudaFreeHost(h_status);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+
+  template <class T>
+  int alloc(T** out, size_t count) {
+    void* p = nullptr;
+    const cudaError_t err = cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T));
+    if (err != cudaSuccess)
+      return fail(UT_ERR_RUNTIME, "cudaMalloc(%zu bytes) failed: %s", count * sizeof(T), cudaGetErrorString(err));
+    allocs.push_back(p);
+    *out = static_cast<T*>(p);
+    return UT_OK;
+  }
+
+  DevConfig& cfg(int64_t e) { return dcfgs[cfg_of_env.empty() ? 0 : cfg_of_env[(size_t)e]]; }
+  int64_t rec_at(int64_t e) const { return rec_off[(size_t)e]; }
+  int64_t set_at(int64_t e) const { return set_off[(size_t)e]; }
+
+  int check_status(const char* what) {
+    UT_CUDA(cudaMemcpyAsync(h_status, d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    UT_CUDA(cudaStreamSynchronize(stream));
+    UT_CUDA(cudaGetLastError());
+    if (h_status[0] == ST_SPAWN_INFEASIBLE) {
+      const ut_env_config& c = cfgs[0];
+      return fail(UT_ERR_CONFIG, "%s: spawn infeasible after 1000 attempts: %d entities with separation in [%g, %g] m",
+                  what, c.n_agents + c.n_targets, c.spawn_min_sep, c.spawn_max_sep);
+    }
+    return UT_OK;
+  }
+
+  int reset_status() {
+    const int32_t init[2] = {0, INT_MAX};
+    UT_CUDA(cudaMemcpyAsync(d_status, init, sizeof init, cudaMemcpyHostToDevice, stream));
+    return UT_OK;
+  }
+
+  int launch_step(int mode) {
+    step_kernel<kPPT><<<(unsigned)n_envs, nt, smem, stream>>>(B, mode, d_status);
+    ++launches;
+    UT_CUDA(cudaGetLastError());
+    return UT_OK;
+  }
+  int launch_reset(int ctor) {
+    reset_kernel<kPPT><<<(unsigned)n_envs, nt, smem, stream>>>(B, ctor, d_status);
+    ++launches;
+    UT_CUDA(cudaGetLastError());
+    return UT_OK;
+  }
+};
+
+namespace {
+
+int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg_of_env, int64_t n_envs,
+          uint64_t seed, int64_t offset, int device) {
+  if (n_envs < 1) return fail(UT_ERR_CONFIG, "vecenv: n_envs must be >= 1");
+  if (n_envs > INT_MAX) return fail(UT_ERR_CONFIG, "vecenv: n_envs must fit a CUDA grid");
+  v->device = device;
+  v->n_envs = n_envs;
+  v->offset = offset;
+  v->seed = seed;
+  for (int i = 0; i < n_cfg; ++i) {
+    ut_env_config c = cfgs[i];
+    const int rc = ut_config_finalize(&c);
+    if (rc) return rc;
+    if (c.pf.n_particles > kMaxParticles)
+      return fail(UT_ERR_CONFIG, "env.pf.n_particles must be <= %d on this device build", kMaxParticles);
+    if (i > 0 && c.pf.n_particles != cfgs[0].pf.n_particles)
+      return fail(UT_ERR_CONFIG, "mixed fleets must share env.pf.n_particles");
+    v->cfgs.push_back(c);
+    v->dcfgs.push_back(to_dev(c));
+  }
+  if (cfg_of_env) {
+    v->cfg_of_env.assign(cfg_of_env, cfg_of_env + n_envs);
+    for (int32_t k : v->cfg_of_env)
+      if (k < 0 || k >= n_cfg) return fail(UT_ERR_CONFIG, "cfg_of_env index %d out of range", k);
+  }
+  for (const DevConfig& d : v->dcfgs) {
+    v->A_max = std::max(v->A_max, d.A);
+    v->T_max = std::max(v->T_max, d.T);
+    v->R_max = std::max(v->R_max, d.R);
+    v->rec_words_max = std::max(v->rec_words_max, d.rec_words);
+  }
+  v->P = v->dcfgs[0].P;
+  v->rec_off.resize((size_t)n_envs);
+  v->set_off.resize((size_t)n_envs);
+  for (int64_t e = 0; e < n_envs; ++e) {
+    const DevConfig& d = v->cfg(e);
+    v->rec_off[(size_t)e] = v->total_rec;
+    v->set_off[(size_t)e] = v->total_sets;
+    v->total_rec += d.rec_words;
+    v->total_sets += (int64_t)d.A * d.T;
+  }
+
+  UT_CUDA(cudaSetDevice(device));
+  UT_CUDA(cudaStreamCreateWithFlags(&v->own_stream, cudaStreamNonBlocking));
+  v->stream = v->own_stream;
+  UT_CUDA(cudaMallocHost(&v->h_status, 2 * sizeof(int32_t)));
+
+  DevBatch& B = v->B;
+  B.n_envs = n_envs;
+  B.env_index_offset = offset;
+  B.seed = seed;
+  B.n_cfg = n_cfg;
+  B.A_max = v->A_max;
+  B.T_max = v->T_max;
+  B.R_max = v->R_max;
+  B.P = v->P;
+  const int64_t P = v->P, Am = v->A_max, Rm = v->R_max, Tm = v->T_max;
+  B.obs_rows = n_envs * Am * Rm;
+  B.global_rows = n_envs * Rm;
+  int rc;
+  DevConfig* dc;
+  if ((rc = v->alloc(&dc, v->dcfgs.size()))) return rc;
+  UT_CUDA(cudaMemcpy(dc, v->dcfgs.data(), sizeof(DevConfig) * v->dcfgs.size(), cudaMemcpyHostToDevice));
+  B.cfgs = dc;
+  if (!v->cfg_of_env.empty()) {
+    int32_t* ce;
+    int64_t *ro, *so;
+    if ((rc = v->alloc(&ce, (size_t)n_envs))) return rc;
+    if ((rc = v->alloc(&ro, (size_t)n_envs))) return rc;
+    if ((rc = v->alloc(&so, (size_t)n_envs))) return rc;
+    UT_CUDA(cudaMemcpy(ce, v->cfg_of_env.data(), sizeof(int32_t) * n_envs, cudaMemcpyHostToDevice));
+    UT_CUDA(cudaMemcpy(ro, v->rec_off.data(), sizeof(int64_t) * n_envs, cudaMemcpyHostToDevice));
+    UT_CUDA(cudaMemcpy(so, v->set_off.data(), sizeof(int64_t) * n_envs, cudaMemcpyHostToDevice));
+    B.cfg_of_env = ce;
+    B.rec_offset = ro;
+    B.set_offset = so;
+  }
+  const size_t np = (size_t)(v->total_sets * P);
+  if ((rc = v->alloc(&B.rec, (size_t)v->total_rec))) return rc;
+  if ((rc = v->alloc(&B.px, np))) return rc;
+  if ((rc = v->alloc(&B.py, np))) return rc;
+  if ((rc = v->alloc(&B.vx, np))) return rc;
+  if ((rc = v->alloc(&B.vy, np))) return rc;
+  if ((rc = v->alloc(&B.w, np))) return rc;
+  if ((rc = v->alloc(&B.obs, (size_t)(12 * B.obs_rows)))) return rc;
+  if ((rc = v->alloc(&B.final_obs, (size_t)(12 * B.obs_rows)))) return rc;
+  if ((rc = v->alloc(&B.global, (size_t)(12 * B.global_rows)))) return rc;
+  if ((rc = v->alloc(&B.rewards, (size_t)n_envs))) return rc;
+  if ((rc = v->alloc(&B.dones, (size_t)n_envs))) return rc;
+  if ((rc = v->alloc(&B.masks, (size_t)(n_envs * Am * 5)))) return rc;
+  if ((rc = v->alloc(&B.track_err, (size_t)(n_envs * Tm)))) return rc;
+  if ((rc = v->alloc(&B.min_dist, (size_t)(n_envs * Tm)))) return rc;
+  if ((rc = v->alloc(&B.lost, (size_t)(n_envs * Tm)))) return rc;
+  if ((rc = v->alloc(&B.collision, (size_t)n_envs))) return rc;
+  if ((rc = v->alloc(&B.step, (size_t)n_envs))) return rc;
+  int32_t* acts;
+  if ((rc = v->alloc(&acts, (size_t)(n_envs * Am)))) return rc;
+  B.actions = acts;
+  if ((rc = v->alloc(&v->d_status, 2))) return rc;
+  B.error_env = v->d_status + 1;
+  B.error_info = nullptr;
+  // VecEnv ctor zero-fills every batch buffer (vecenv.cpp:26-38)
+  UT_CUDA(cudaMemsetAsync(B.final_obs, 0, sizeof(double) * 12 * B.obs_rows, v->stream));
+  UT_CUDA(cudaMemsetAsync(B.track_err, 0, sizeof(double) * n_envs * Tm, v->stream));
+  UT_CUDA(cudaMemsetAsync(B.min_dist, 0, sizeof(double) * n_envs * Tm, v->stream));
+  UT_CUDA(cudaMemsetAsync(B.lost, 0, n_envs * Tm, v->stream));
+  UT_CUDA(cudaMemsetAsync(B.collision, 0, n_envs, v->stream));
+  UT_CUDA(cudaMemsetAsync(acts, 0, sizeof(int32_t) * n_envs * Am, v->stream));
+
+  v->nt = threads_for(v->P);
+  v->smem = smem_bytes(v->rec_words_max, v->A_max, v->T_max, v->P);
+  int max_optin = 0;
+  UT_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  if ((int)v->smem > max_optin)
+    return fail(UT_ERR_CONFIG, "configuration needs %zu B of shared memory per env (max %d)", v->smem, max_optin);
+  UT_CUDA(cudaFuncSetAttribute(step_kernel<kPPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
+  UT_CUDA(cudaFuncSetAttribute(reset_kernel<kPPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
+  UT_CUDA(cudaFuncSetAttribute(tokens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(sizeof(double) * v->rec_words_max)));
+
+  // Environment ctors: pf::init draws, then spawn (env.cpp:110-151)
+  if ((rc = v->reset_status())) return rc;
+  if ((rc = v->launch_reset(1))) return rc;
+  return v->check_status("vecenv ctor");
+}
+
+int host_rudders(ut_vecenv* v, int64_t e, std::vector<double>& out) {
+  const DevConfig& d = v->cfg(e);
+  out.resize((size_t)d.A);
+  UT_CUDA(cudaMemcpy(out.data(), v->B.rec + v->rec_at(e) + d.o_agent + V_RUDDER * d.A, sizeof(double) * d.A,
+                     cudaMemcpyDeviceToHost));
+  return UT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ut_abi_version(void) { return UT_ABI_VERSION; }
+const char* ut_last_error(void) { return g_err.c_str(); }
+
+void ut_config_default(ut_env_config* c) {
+  std::memset(c, 0, sizeof *c);
+  c->n_agents = 1;
+  c->n_targets = 1;
+  c->horizon = 128;
+  c->dt = 30.0;
+  c->agent_speed = 1.0;
+  c->target_speed_frac = 0.3;
+  c->target_speed_frac_max = 0.0;
+  c->target_turn_interval = 20.0;
+  c->detection_range = 450.0;
+  c->comm_range = 1500.0;
+  c->comm_drop_prob = 0.1;
+  c->range_noise_std = 3.0;
+  c->eps_min = 10.0;
+  c->eps_max = 50.0;
+  c->d_min = 50.0;
+  c->d_safe = 10.0;
+  c->reward_mode = UT_REWARD_TRACKING;
+  c->spawn_min_sep = 50.0;
+  c->spawn_max_sep = 200.0;
+  c->perturbation_std = 0.0;
+  c->target_depth_min = 10.0;
+  c->target_depth_max = 60.0;
+  c->lost_steps = 20;
+  c->heading_model_kind = UT_HEADING_DEFAULT;
+  c->heading_noise_std = 0.02;
+  c->pf.n_particles = 1024;
+  c->pf.process_noise_pos = 1.0;
+  c->pf.process_noise_vel = 0.05;
+  c->pf.speed_margin = 1.2;
+  c->pf.init_radius = 450.0;
+}
+
+int ut_config_finalize(ut_env_config* c) {
+  if (c->heading_noise_std < 0.0) return fail(UT_ERR_CONFIG, "heading model noise_std must be >= 0");
+  if (c->n_agents < 1) return fail(UT_ERR_CONFIG, "env.n_agents must be >= 1");
+  if (c->n_targets < 1) return fail(UT_ERR_CONFIG, "env.n_targets must be >= 1");
+  if (c->horizon < 1) return fail(UT_ERR_CONFIG, "env.horizon must be >= 1");
+  if (!(c->dt > 0.0)) return fail(UT_ERR_CONFIG, "env.dt must be > 0");
+  if (!(c->agent_speed > 0.0)) return fail(UT_ERR_CONFIG, "env.agent_speed must be > 0");
+  if (c->target_speed_frac < 0.0) return fail(UT_ERR_CONFIG, "env.target_speed_frac must be >= 0");
+  if (c->target_turn_interval < 1.0) return fail(UT_ERR_CONFIG, "env.target_turn_interval must be >= 1 step");
+  if (c->eps_min >= c->eps_max) return fail(UT_ERR_CONFIG, "env.eps_min must be < env.eps_max");
+  if (c->spawn_min_sep >= c->spawn_max_sep)
+    return fail(UT_ERR_CONFIG, "env.spawn_min_sep must be < env.spawn_max_sep");
+  if (c->comm_drop_prob < 0.0 || c->comm_drop_prob > 1.0)
+    return fail(UT_ERR_CONFIG, "env.comm_drop_prob must be in [0, 1]");
+  if (c->range_noise_std < 0.0) return fail(UT_ERR_CONFIG, "env.range_noise_std must be >= 0");
+  if (c->target_depth_min < 0.0 || c->target_depth_max < c->target_depth_min)
+    return fail(UT_ERR_CONFIG, "env.target_depth band must satisfy 0 <= min <= max");
+  if (c->lost_steps < 1) return fail(UT_ERR_CONFIG, "env.lost_steps must be >= 1");
+  if (c->pf.n_particles < 1) return fail(UT_ERR_CONFIG, "env.pf.n_particles must be >= 1");
+  if (!(c->pf.init_radius > 0.0)) return fail(UT_ERR_CONFIG, "env.pf.init_radius must be > 0");
+  if (c->heading_model_kind == UT_HEADING_DEFAULT) {
+    double a, b;
+    if (!default_bucket(c->agent_speed, c->dt, &a, &b))
+      return fail(UT_ERR_CONFIG, "heading model has no bucket for (speed=%g m/s, dt=%g s)", c->agent_speed, c->dt);
+    c->heading_a = a;
+    c->heading_b = b;
+  } else if (c->heading_model_kind != UT_HEADING_BUCKET) {
+    return fail(UT_ERR_CONFIG, "env.heading_model_kind must be 0 (default) or 1 (bucket)");
+  }
+  c->max_turn_per_step = std::fabs(c->heading_a * 0.24 + c->heading_b);  // env.cpp:115-116
+  return UT_OK;
+}
+
+int ut_vecenv_create(const ut_env_config* cfg, int64_t n_envs, uint64_t master_seed, int64_t env_index_offset,
+                     int device, ut_vecenv** out) {
+  *out = nullptr;
+  auto* v = new ut_vecenv();
+  const int rc = build(v, cfg, 1, nullptr, n_envs, master_seed, env_index_offset, device);
+  if (rc) {
+    const std::string msg = g_err;
+    delete v;
+    g_err = msg;
+    return rc;
+  }
+  *out = v;
+  return UT_OK;
+}
+
+int ut_vecenv_create_mixed(const ut_env_config* cfgs, int32_t n_cfgs, const int32_t* cfg_of_env, int64_t n_envs,
+                           uint64_t master_seed, int64_t env_index_offset, int device, ut_vecenv** out) {
+  *out = nullptr;
+  if (n_cfgs < 1 || !cfg_of_env) return fail(UT_ERR_CONFIG, "mixed vecenv needs >= 1 config and a cfg_of_env map");
+  auto* v = new ut_vecenv();
+  const int rc = build(v, cfgs, n_cfgs, cfg_of_env, n_envs, master_seed, env_index_offset, device);
+  if (rc) {
+    const std::string msg = g_err;
+    delete v;
+    g_err = msg;
+    return rc;
+  }
+  *out = v;
+  return UT_OK;
+}
+
+void ut_vecenv_destroy(ut_vecenv* v) { delete v; }
+
+int ut_vecenv_reset_all(ut_vecenv* v) {
+  int rc;
+  if ((rc = v->reset_status()) || (rc = v->launch_reset(0))) return rc;
+  return v->check_status("reset_all");
+}
+
+int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device) {
+  const size_t n = (size_t)(v->n_envs * v->A_max);
+  UT_CUDA(cudaMemcpyAsync(const_cast<int32_t*>(v->B.actions), actions, n * sizeof(int32_t),
+                          actions_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, v->stream));
+  int rc;
+  if ((rc = v->reset_status())) return rc;
+  const int tpb = 256;
+  validate_kernel<<<(unsigned)((v->n_envs + tpb - 1) / tpb), tpb, 0, v->stream>>>(v->B);
+  ++v->launches;
+  UT_CUDA(cudaGetLastError());
+  UT_CUDA(cudaMemcpyAsync(v->h_status, v->d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, v->stream));
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  if (v->h_status[1] != INT_MAX) {
+    // message format of env.cpp:241-246 prefixed like vecenv.cpp:88-93
+    const int64_t e = v->h_status[1];
+    std::vector<int32_t> acts((size_t)v->A_max);
+    UT_CUDA(cudaMemcpy(acts.data(), v->B.actions + e * v->A_max, sizeof(int32_t) * v->A_max, cudaMemcpyDeviceToHost));
+    std::vector<double> rud;
+    if ((rc = host_rudders(v, e, rud))) return rc;
+    for (int a = 0; a < v->cfg(e).A; ++a) {
+      const int act = acts[(size_t)a], r = (int)rud[(size_t)a];
+      if (act < 0 || act >= UT_NUM_ACTIONS || std::abs(act - r) > 1)
+        return fail(UT_ERR_CONTRACT, "env %lld: step: invalid action %d for agent %d at rudder index %d", (long long)e,
+                    act, a, r);
+    }
+    return fail(UT_ERR_CONTRACT, "env %lld: step: invalid action", (long long)e);
+  }
+  if ((rc = v->launch_step(MODE_EXTERNAL))) return rc;
+  return v->check_status("step");
+}
+
+int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps) {
+  if (policy != UT_POLICY_RANDOM && policy != UT_POLICY_SCRIPTED)
+    return fail(UT_ERR_CONTRACT, "step_policy: unknown policy %d", policy);
+  int rc;
+  if ((rc = v->reset_status())) return rc;
+  for (int i = 0; i < n_steps; ++i)
+    if ((rc = v->launch_step(policy == UT_POLICY_RANDOM ? MODE_RANDOM : MODE_SCRIPTED))) return rc;
+  return v->check_status("step_policy");
+}
+
+int ut_vecenv_refresh_outputs(ut_vecenv* v) {
+  tokens_kernel<<<(unsigned)v->n_envs, 64, sizeof(double) * v->rec_words_max, v->stream>>>(v->B);
+  ++v->launches;
+  UT_CUDA(cudaGetLastError());
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  return UT_OK;
+}
+
+int ut_vecenv_buffers(ut_vecenv* v, ut_buffers* o) {
+  const DevBatch& B = v->B;
+  o->n_envs = v->n_envs;
+  o->n_agents = v->A_max;
+  o->n_targets = v->T_max;
+  o->n_rows = v->R_max;
+  o->n_particles = v->P;
+  o->obs_rows = B.obs_rows;
+  o->global_rows = B.global_rows;
+  o->obs = B.obs;
+  o->final_obs = B.final_obs;
+  o->global_state = B.global;
+  o->rewards = B.rewards;
+  o->dones = B.dones;
+  o->masks = B.masks;
+  o->tracking_error = B.track_err;
+  o->min_agent_dist = B.min_dist;
+  o->target_lost = B.lost;
+  o->collision = B.collision;
+  o->step = B.step;
+  o->actions = const_cast<int32_t*>(B.actions);
+  o->px = B.px;
+  o->py = B.py;
+  o->vx = B.vx;
+  o->vy = B.vy;
+  o->w = B.w;
+  return UT_OK;
+}
+
+int ut_vecenv_copy_outputs(ut_vecenv* v, const ut_host_outputs* d) {
+  const DevBatch& B = v->B;
+  const int64_t n = v->n_envs, Am = v->A_max, Tm = v->T_max;
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!dst) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, v->stream);
+  };
+  UT_CUDA(cp(d->obs, B.obs, sizeof(double) * 12 * B.obs_rows));
+  UT_CUDA(cp(d->final_obs, B.final_obs, sizeof(double) * 12 * B.obs_rows));
+  UT_CUDA(cp(d->global_state, B.global, sizeof(double) * 12 * B.global_rows));
+  UT_CUDA(cp(d->rewards, B.rewards, sizeof(double) * n));
+  UT_CUDA(cp(d->dones, B.dones, (size_t)n));
+  UT_CUDA(cp(d->masks, B.masks, (size_t)(n * Am * 5)));
+  UT_CUDA(cp(d->tracking_error, B.track_err, sizeof(double) * n * Tm));
+  UT_CUDA(cp(d->min_agent_dist, B.min_dist, sizeof(double) * n * Tm));
+  UT_CUDA(cp(d->target_lost, B.lost, (size_t)(n * Tm)));
+  UT_CUDA(cp(d->collision, B.collision, (size_t)n));
+  UT_CUDA(cp(d->step, B.step, sizeof(int32_t) * n));
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  return UT_OK;
+}
+
+int ut_vecenv_set_stream(ut_vecenv* v, void* s) {
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  v->stream = s ? static_cast<cudaStream_t>(s) : v->own_stream;
+  return UT_OK;
+}
+
+int ut_vecenv_synchronize(ut_vecenv* v) {
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  return UT_OK;
+}
+
+int ut_vecenv_stats(ut_vecenv* v, double out[UT_N_STATS], int reset) {
+  double* d;
+  UT_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * UT_N_STATS, v->stream));
+  stats_kernel<<<1, 256, 0, v->stream>>>(v->B, d, reset);
+  ++v->launches;
+  UT_CUDA(cudaGetLastError());
+  UT_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * UT_N_STATS, cudaMemcpyDeviceToHost, v->stream));
+  UT_CUDA(cudaFreeAsync(d, v->stream));
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  return UT_OK;
+}
+
+int64_t ut_vecenv_launch_count(const ut_vecenv* v) { return v->launches; }
+
+// Environment::serialize_state (env.cpp:550-593)
+int ut_env_serialize(ut_vecenv* v, int64_t e, double* blob, size_t cap, size_t* len) {
+  if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "serialize: env %lld out of range", (long long)e);
+  const DevConfig& d = v->cfg(e);
+  const int A = d.A, T = d.T, P = d.P, AA = A * A, AT = A * T;
+  const size_t need = (size_t)(5 + 6 * A + 9 * T + A * (6 * A + T * (9 + 5 * P)));
+  *len = need;
+  if (!blob) return UT_OK;
+  if (cap < need) return fail(UT_ERR_DATA, "serialize: buffer of %zu doubles too small (need %zu)", cap, need);
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  std::vector<double> rec((size_t)d.rec_words);
+  UT_CUDA(cudaMemcpy(rec.data(), v->B.rec + v->rec_at(e), sizeof(double) * d.rec_words, cudaMemcpyDeviceToHost));
+  const size_t nset = (size_t)AT * P;
+  std::vector<double> f[5];
+  double* src[5] = {v->B.px, v->B.py, v->B.vx, v->B.vy, v->B.w};
+  for (int k = 0; k < 5; ++k) {
+    f[k].resize(nset);
+    UT_CUDA(cudaMemcpy(f[k].data(), src[k] + (size_t)v->set_at(e) * P, sizeof(double) * nset, cudaMemcpyDeviceToHost));
+  }
+  const double* ag = rec.data() + d.o_agent;
+  const double* tg = rec.data() + d.o_target;
+  const double* info = rec.data() + d.o_info;
+  const double* trk = rec.data() + d.o_track;
+  size_t i = 0;
+  blob[i++] = rec[R_STEP];
+  blob[i++] = rec[R_EP_SPEED];
+  blob[i++] = rec[R_ENV_POS];
+  blob[i++] = rec[R_ENV_HAVE_SPARE];
+  blob[i++] = rec[R_ENV_SPARE];
+  for (int a = 0; a < A; ++a)
+    for (int fl = 0; fl < 6; ++fl) blob[i++] = ag[fl * A + a];
+  for (int t = 0; t < T; ++t)
+    for (int fl = 0; fl < 8; ++fl) blob[i++] = tg[fl * T + t];
+  for (int t = 0; t < T; ++t) blob[i++] = rec[(size_t)d.o_miss + t];
+  for (int a = 0; a < A; ++a) {
+    for (int j = 0; j < A; ++j)
+      for (int fl = 0; fl < I_NFIELD; ++fl) blob[i++] = info[fl * AA + a * A + j];
+    for (int t = 0; t < T; ++t) {
+      const int si = a * T + t;
+      for (int fl = 0; fl < K_NFIELD; ++fl) blob[i++] = trk[fl * AT + si];
+      for (int k = 0; k < 5; ++k) {
+        std::memcpy(blob + i, f[k].data() + (size_t)si * P, sizeof(double) * P);
+        i += (size_t)P;
+      }
+    }
+  }
+  return UT_OK;
+}
+
+// Environment::deserialize_state (env.cpp:595-659). Like the reference, the batch
+// buffers are refreshed only by ut_vecenv_refresh_outputs().
+int ut_env_deserialize(ut_vecenv* v, int64_t e, const double* blob, size_t len) {
+  if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "deserialize: env %lld out of range", (long long)e);
+  const DevConfig& d = v->cfg(e);
+  const int A = d.A, T = d.T, P = d.P, AA = A * A, AT = A * T;
+  const size_t need = (size_t)(5 + 6 * A + 9 * T + A * (6 * A + T * (9 + 5 * P)));
+  if (len < need) return fail(UT_ERR_DATA, "environment state blob truncated");
+  if (len > need) return fail(UT_ERR_DATA, "environment state blob has trailing data");
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  std::vector<double> rec((size_t)d.rec_words);
+  UT_CUDA(cudaMemcpy(rec.data(), v->B.rec + v->rec_at(e), sizeof(double) * d.rec_words, cudaMemcpyDeviceToHost));
+  double* ag = rec.data() + d.o_agent;
+  double* tg = rec.data() + d.o_target;
+  double* info = rec.data() + d.o_info;
+  double* trk = rec.data() + d.o_track;
+  const size_t nset = (size_t)AT * P;
+  std::vector<double> f[5];
+  for (auto& x : f) x.resize(nset);
+  size_t i = 0;
+  // integer fields go through the same (int) truncation as the reference
+  auto as_int = [](double x) { return (double)(int)x; };
+  rec[R_STEP] = as_int(blob[i++]);
+  rec[R_EP_SPEED] = blob[i++];
+  rec[R_ENV_POS] = (double)(uint64_t)blob[i++];
+  rec[R_ENV_HAVE_SPARE] = blob[i++] != 0.0 ? 1.0 : 0.0;
+  rec[R_ENV_SPARE] = blob[i++];
+  for (int a = 0; a < A; ++a)
+    for (int fl = 0; fl < 6; ++fl) {
+      const double x = blob[i++];
+      ag[fl * A + a] = fl == V_RUDDER ? as_int(x) : x;
+    }
+  for (int t = 0; t < T; ++t)
+    for (int fl = 0; fl < 8; ++fl) {
+      const double x = blob[i++];
+      tg[fl * T + t] = (fl == V_RUDDER || fl == V_COUNTDOWN) ? as_int(x) : x;
+    }
+  for (int t = 0; t < T; ++t) rec[(size_t)d.o_miss + t] = as_int(blob[i++]);
+  for (int a = 0; a < A; ++a) {
+    for (int j = 0; j < A; ++j)
+      for (int fl = 0; fl < I_NFIELD; ++fl) {
+        const double x = blob[i++];
+        double& dst = info[fl * AA + a * A + j];
+        dst = fl == I_AGE ? as_int(x) : fl == I_VALID ? (x != 0.0 ? 1.0 : 0.0) : x;
+      }
+    for (int t = 0; t < T; ++t) {
+      const int si = a * T + t;
+      for (int fl = 0; fl < K_NFIELD; ++fl) {
+        const double x = blob[i++];
+        double& dst = trk[fl * AT + si];
+        dst = fl == K_AGE ? as_int(x)
+              : (fl == K_EVER || fl == K_HAVE_SPARE) ? (x != 0.0 ? 1.0 : 0.0)
+              : fl == K_POS ? (double)(uint64_t)x
+                            : x;
+      }
+      for (int k = 0; k < 5; ++k) {
+        std::memcpy(f[k].data() + (size_t)si * P, blob + i, sizeof(double) * P);
+        i += (size_t)P;
+      }
+    }
+  }
+  UT_CUDA(cudaMemcpy(v->B.rec + v->rec_at(e), rec.data(), sizeof(double) * d.rec_words, cudaMemcpyHostToDevice));
+  double* dst[5] = {v->B.px, v->B.py, v->B.vx, v->B.vy, v->B.w};
+  for (int k = 0; k < 5; ++k)
+    UT_CUDA(cudaMemcpy(dst[k] + (size_t)v->set_at(e) * P, f[k].data(), sizeof(double) * nset, cudaMemcpyHostToDevice));
+  return UT_OK;
+}
+
+int ut_env_world_step(ut_vecenv* v, int64_t e, int32_t* step) {
+  if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "world_step: env %lld out of range", (long long)e);
+  double s = 0.0;
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  UT_CUDA(cudaMemcpy(&s, v->B.rec + v->rec_at(e) + R_STEP, sizeof(double), cudaMemcpyDeviceToHost));
+  *step = (int32_t)s;
+  return UT_OK;
+}
+
+// benchmark_sps (vecenv.cpp:175-202): warmup, then CUDA-event-timed steps.
+int ut_benchmark_sps(const ut_env_config* cfg, int64_t n_envs, int32_t n_steps, int policy, uint64_t seed,
+                     int32_t warmup, int device, ut_benchmark_report* out) {
+  ut_vecenv* v = nullptr;
+  int rc = ut_vecenv_create(cfg, n_envs, seed, 0, device, &v);
+  if (rc) return rc;
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  rc = ut_vecenv_step_policy(v, policy, warmup);
+  if (!rc) {
+    cudaEventRecord(t0, v->stream);
+    rc = ut_vecenv_step_policy(v, policy, n_steps);
+    cudaEventRecord(t1, v->stream);
+    cudaEventSynchronize(t1);
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (!rc) {
+    out->n_envs = n_envs;
+    out->n_agents = v->A_max;
+    out->n_targets = v->T_max;
+    out->timed_steps = n_steps;
+    out->wall_seconds = ms / 1e3;
+    out->sps = (double)n_envs * n_steps / out->wall_seconds;
+    out->agent_sps = out->sps * v->A_max;
+  }
+  ut_vecenv_destroy(v);
+  return rc;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ ut_debug.h ---
+namespace {
+__global__ void cr_grid_kernel(int kind, float* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (1u << 24)) return;
+  const float two_pi_f = 2.0f * 3.14159265358979323846f;
+  if (kind == 0) {
+    out[i] = cr_logf((float)(i + 1u) * 0x1.0p-24f);
+  } else {
+    float s, c;
+    cr_sincosf(__fmul_rn(two_pi_f, (float)i * 0x1.0p-24f), &s, &c);
+    out[i] = kind == 1 ? c : s;
+  }
+}
+__global__ void philox_kernel(uint64_t key, uint64_t stream, uint64_t block0, int n, uint4* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = philox(key, stream, block0 + (uint64_t)i);
+}
+__global__ void derive_key_kernel(uint64_t a, uint64_t b, uint64_t c, uint64_t d, uint64_t* out) {
+  *out = derive_key(a, b, c, d);
+}
+}  // namespace
+
+#include "ut_debug.h"
+
+extern "C" {
+int ut_debug_abi_sizes(int64_t out[4]) {
+  out[0] = sizeof(ut_env_config);
+  out[1] = sizeof(ut_buffers);
+  out[2] = sizeof(ut_host_outputs);
+  out[3] = sizeof(ut_benchmark_report);
+  return UT_OK;
+}
+int ut_debug_cr_grid(int kind, int device, float* host_out) {
+  UT_CUDA(cudaSetDevice(device));
+  float* d = nullptr;
+  const size_t n = (size_t)1 << 24;
+  UT_CUDA(cudaMalloc(&d, n * sizeof(float)));
+  cr_grid_kernel<<<(unsigned)(n / 256), 256>>>(kind, d);
+  cudaError_t err = cudaMemcpy(host_out, d, n * sizeof(float), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  UT_CUDA(err);
+  return UT_OK;
+}
+int ut_debug_philox(uint64_t key, uint64_t stream, uint64_t block0, int32_t n, int device, uint32_t* host_out) {
+  UT_CUDA(cudaSetDevice(device));
+  uint4* d = nullptr;
+  UT_CUDA(cudaMalloc(&d, (size_t)n * sizeof(uint4)));
+  philox_kernel<<<(unsigned)((n + 255) / 256), 256>>>(key, stream, block0, n, d);
+  cudaError_t err = cudaMemcpy(host_out, d, (size_t)n * sizeof(uint4), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  UT_CUDA(err);
+  return UT_OK;
+}
+int ut_debug_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t dd, int device, uint64_t* out) {
+  UT_CUDA(cudaSetDevice(device));
+  uint64_t* d = nullptr;
+  UT_CUDA(cudaMalloc(&d, sizeof(uint64_t)));
+  derive_key_kernel<<<1, 1>>>(a, b, c, dd, d);
+  cudaError_t err = cudaMemcpy(out, d, sizeof(uint64_t), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  UT_CUDA(err);
+  return UT_OK;
+}
+}  // extern "C"

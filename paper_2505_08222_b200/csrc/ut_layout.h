@@ -1,0 +1,95 @@
+// ut_layout.h -- device state-store layout shared by host and device code.
+//
+// HBM holds three things:
+//  1. the particle store, structure-of-arrays: px/py/vx/vy/w each [set][P] fp64,
+//     set = set_offset[env] + agent * T + target -- one 8 KB contiguous chunk per
+//     set and field at P = 1024 (ParticleSet, tracking.hpp:39-55);
+//  2. one env record per env (rec_offset[env], `rec_words` fp64 words): every
+//     other piece of Environment state (env.hpp:44-51, 131-171) as small SoA
+//     arrays inside the record, staged whole through shared memory by the CTA
+//     that steps the env. Integer fields are stored as exact fp64 values, like
+//     the reference's own state blob (env.cpp:550-593);
+//  3. the batch output buffers of VecEnv (vecenv.hpp:51-62), column-major.
+#pragma once
+#include <stdint.h>
+
+namespace ut {
+
+// record scalar slots
+enum : int {
+  R_STEP = 0,
+  R_EP_SPEED = 1,
+  R_ENV_POS = 2,
+  R_ENV_HAVE_SPARE = 3,
+  R_ENV_SPARE = 4,
+  R_BENCH_POS = 5,
+  R_EP_RETURN = 6,
+  R_LAST_DONE = 7,
+  R_NSCALAR = 8
+};
+// vehicle fields (agents: first 6; targets: all 8)
+enum : int { V_X = 0, V_Y, V_Z, V_HEAD, V_SPEED, V_RUDDER, V_COUNTDOWN, V_CMD };
+// AgentInfo fields (env.hpp:19-25)
+enum : int { I_X = 0, I_Y, I_Z, I_HEAD, I_AGE, I_VALID, I_NFIELD };
+// track fields: TrackEstimate + ever_measured + PF RngStream::State + max_speed
+enum : int { K_EX = 0, K_EY, K_SPREAD, K_AGE, K_EVER, K_POS, K_HAVE_SPARE, K_SPARE, K_MAXSPEED, K_NFIELD };
+
+constexpr int kStatCount = 9;  // ut_env.h UT_N_STATS
+
+// Resolved configuration for one fleet shape (EnvConfig after finalize()).
+struct DevConfig {
+  int A, T, R, P;
+  int horizon, reward_mode, lost_steps, noise_on;
+  double dt, agent_speed, tgt_lo, tgt_hi, turn_interval;
+  double det_range, comm_range, drop, range_noise, sigma_meas;
+  double eps_min, eps_max, d_min, d_safe;
+  double min_sep, disc_r, pert_std, depth_min, depth_max;
+  double pn, vn, speed_margin, init_radius;
+  double head_a, head_b, head_noise, max_turn;
+  // record layout (fp64 word offsets)
+  int o_agent, o_target, o_miss, o_info, o_track, o_stats, rec_words, _pad;
+};
+
+__host__ __device__ inline void layout_config(DevConfig& c) {
+  c.R = c.A + c.T;
+  c.o_agent = R_NSCALAR;
+  c.o_target = c.o_agent + 6 * c.A;
+  c.o_miss = c.o_target + 8 * c.T;
+  c.o_info = c.o_miss + c.T;
+  c.o_track = c.o_info + I_NFIELD * c.A * c.A;
+  c.o_stats = c.o_track + K_NFIELD * c.A * c.T;
+  c.rec_words = (c.o_stats + kStatCount + 1) & ~1;
+}
+
+// Per-batch constant tables (device pointers) passed to every kernel.
+struct DevBatch {
+  int64_t n_envs;
+  int64_t env_index_offset;  // global index of env 0 (RNG key)
+  uint64_t seed;
+  int n_cfg;
+  int A_max, T_max, R_max, P;
+  const DevConfig* cfgs;      // [n_cfg]
+  const int32_t* cfg_of_env;  // [n_envs] or nullptr (homogeneous)
+  const int64_t* rec_offset;  // [n_envs] words, or nullptr: env * rec_words(cfg 0)
+  const int64_t* set_offset;  // [n_envs] sets, or nullptr: env * A * T
+  double* rec;
+  double *px, *py, *vx, *vy, *w;
+  // batch outputs
+  int64_t obs_rows, global_rows;
+  double* obs;
+  double* final_obs;
+  double* global;
+  double* rewards;
+  uint8_t* dones;
+  uint8_t* masks;
+  double* track_err;
+  double* min_dist;
+  uint8_t* lost;
+  uint8_t* collision;
+  int32_t* step;
+  const int32_t* actions;
+  int32_t* error_env;  // validation: lowest failing env (INT32_MAX if none)
+  int32_t* error_info; // [3] agent, action, rudder of that env
+};
+
+}  // namespace ut

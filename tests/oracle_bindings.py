@@ -59,6 +59,8 @@ def oracle_lib():
             getattr(lib, f).restype = C.c_float
         lib.uto_fill_normals.argtypes = [U64, U64, U64, I64, C.POINTER(C.c_float)]
         lib.uto_fill_normals.restype = None
+        lib.uto_cr_grid.argtypes = [C.c_int, C.c_void_p]
+        lib.uto_cr_grid.restype = None
         _oracle_lib = lib
     return _oracle_lib
 
