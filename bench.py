@@ -61,8 +61,8 @@ def algorithmic_bytes_per_env_step(A, T, P, rec_words):
 
 def rec_words_for(A, T):
     o_track = 8 + 6 * A + 8 * T + T + 6 * A * A
-    o_stats = o_track + 9 * A * T
-    return (o_stats + 9 + 1) & ~1
+    o_stats = o_track + 10 * A * T
+    return (o_stats + 10 + 1) & ~1
 
 
 class ClockSampler:
@@ -218,6 +218,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2505_08222_b200.vecenv import VecEnv
     from paper_2505_08222_b200.sharding import shard_range
+    from paper_2505_08222_b200._abi import STAT_NAMES
 
     cfg = make_cfg(args.config, args.particles)
     A, T, P = cfg.n_agents, cfg.n_targets, cfg.pf.n_particles
@@ -320,9 +321,7 @@ def main():
                      "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_kind},
         "gpu_launches": gpu_launches,
         "clocks": clocks.summary(),
-        "stats": {k: float(v) for k, v in zip(
-            ("env_steps", "reward_sum", "track_err_sum", "episodes_done", "episode_return_sum",
-             "collision_steps", "lost_target_steps", "pf_updates", "pf_resamples"), st)},
+        "stats": {k: float(v) for k, v in zip(STAT_NAMES, st)},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

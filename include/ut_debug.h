@@ -13,6 +13,11 @@ extern "C" {
 int ut_debug_cr_grid(int kind, int device, float* host_out);
 /* n consecutive Philox4x32-10 blocks from block0 (rng.hpp:116-131): 4n words. */
 int ut_debug_philox(uint64_t key, uint64_t stream, uint64_t block0, int32_t n, int device, uint32_t* host_out);
+struct ut_vecenv;
+/* Verification knobs: force_exact != 0 makes every particle set take the exact
+ * sequential update path (tracking.cpp:119-143 once per measurement) instead of
+ * the merged one; trace_env >= 0 printf's a per-set trace for that env. */
+int ut_debug_set_knobs(struct ut_vecenv* v, int force_exact, int64_t trace_env);
 /* sizeof of the ABI structs as compiled: ut_env_config, ut_buffers,
  * ut_host_outputs, ut_benchmark_report (no device needed). */
 int ut_debug_abi_sizes(int64_t out[4]);

@@ -123,6 +123,7 @@ enum {
   UT_STAT_LOST_TARGET_STEPS,  /* (env, target)-steps flagged lost         */
   UT_STAT_PF_UPDATES,         /* particle-filter measurement updates      */
   UT_STAT_PF_RESAMPLES,       /* particle-filter resamples                */
+  UT_STAT_PF_EXACT_PATH,      /* sets that took the exact sequential update path */
   UT_N_STATS
 };
 
@@ -180,6 +181,15 @@ int ut_vecenv_synchronize(ut_vecenv* v);
 int ut_vecenv_stats(ut_vecenv* v, double out[UT_N_STATS], int reset);
 /* Number of kernels this handle has launched so far. */
 int64_t ut_vecenv_launch_count(const ut_vecenv* v);
+
+/* VecEnv::enable_phase_timing / reset_timing / phase_ns (vecenv.hpp:64-67,
+ * PhaseTimer env.cpp:18-36) on the device: per-env SM clock cycles spent in
+ * UT_PHASE_* summed over envs. The seven reference phases map onto four:
+ * targets+agents+measure+comm decisions -> PROLOGUE; filter + fused comm
+ * updates -> FILTER; observe + reward -> OUTPUT; auto-reset -> RESET. */
+enum { UT_PHASE_PROLOGUE = 0, UT_PHASE_FILTER, UT_PHASE_OUTPUT, UT_PHASE_RESET, UT_N_PHASES };
+int ut_vecenv_enable_phase_timing(ut_vecenv* v, int on);
+int ut_vecenv_phase_cycles(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset);
 
 /* ---- per-env state (Environment API) ----------------------------------- */
 /* Environment::serialize_state / deserialize_state (env.cpp:550-659), identical

@@ -482,6 +482,8 @@ static int pf_maybe_resample(uto_vecenv* v, pfview* p) {
   double s2 = p->w[0] * p->w[0];
   for (int64_t i = 1; i < n; ++i) s2 = s2 + p->w[i] * p->w[i];
   const double ess = 1.0 / s2;
+  if (getenv("UTO_TRACE")) fprintf(stderr, "[oracle] ess=%.17g resample=%d pos=%llu\n", ess, ess < (double)n / 2.0,
+                                   (unsigned long long)p->s->rng.pos);
   if (!(ess < (double)n / 2.0)) return 0;
   const double u0 = uniform(&p->s->rng);
   const double inv_n = 1.0 / (double)n;

@@ -14,7 +14,7 @@ UT_HEADING_DEFAULT, UT_HEADING_BUCKET = 0, 1
 
 STAT_NAMES = (
     "env_steps", "reward_sum", "track_err_sum", "episodes_done", "episode_return_sum",
-    "collision_steps", "lost_target_steps", "pf_updates", "pf_resamples",
+    "collision_steps", "lost_target_steps", "pf_updates", "pf_resamples", "pf_exact_path",
 )
 UT_N_STATS = len(STAT_NAMES)
 
@@ -113,6 +113,8 @@ def declare_product(lib):
         "ut_env_world_step": (C.c_int, [P, I64, C.POINTER(I32)]),
         "ut_benchmark_sps": (C.c_int, [cfgp, I64, I32, C.c_int, U64, I32, C.c_int,
                                        C.POINTER(BenchmarkReport)]),
+        "ut_vecenv_enable_phase_timing": (C.c_int, [P, C.c_int]),
+        "ut_vecenv_phase_cycles": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int]),
         "ut_last_error": (C.c_char_p, []),
         "ut_abi_version": (C.c_int, []),
     }
@@ -133,6 +135,8 @@ def declare_debug(lib):
     lib.ut_debug_derive_key.restype = C.c_int
     lib.ut_debug_abi_sizes.argtypes = [C.POINTER(C.c_int64)]
     lib.ut_debug_abi_sizes.restype = C.c_int
+    lib.ut_debug_set_knobs.argtypes = [C.c_void_p, C.c_int, C.c_int64]
+    lib.ut_debug_set_knobs.restype = C.c_int
     return lib
 
 
@@ -142,5 +146,6 @@ PRODUCT_SYMBOLS = (
     "ut_vecenv_refresh_outputs", "ut_vecenv_buffers", "ut_vecenv_copy_outputs",
     "ut_vecenv_set_stream", "ut_vecenv_synchronize", "ut_vecenv_stats", "ut_vecenv_launch_count",
     "ut_env_serialize", "ut_env_deserialize", "ut_env_world_step", "ut_benchmark_sps",
+    "ut_vecenv_enable_phase_timing", "ut_vecenv_phase_cycles",
     "ut_last_error", "ut_abi_version",
 )

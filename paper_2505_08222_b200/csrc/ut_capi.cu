@@ -301,6 +301,9 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   if ((rc = v->alloc(&v->d_status, 2))) return rc;
   B.error_env = v->d_status + 1;
   B.error_info = nullptr;
+  B.force_exact = 0;
+  B.trace_env = -1;
+  B.phase_cycles = nullptr;
   // VecEnv ctor zero-fills every batch buffer (vecenv.cpp:26-38)
   UT_CUDA(cudaMemsetAsync(B.final_obs, 0, sizeof(double) * 12 * B.obs_rows, v->stream));
   UT_CUDA(cudaMemsetAsync(B.track_err, 0, sizeof(double) * n_envs * Tm, v->stream));
@@ -572,6 +575,32 @@ int ut_vecenv_stats(ut_vecenv* v, double out[UT_N_STATS], int reset) {
 
 int64_t ut_vecenv_launch_count(const ut_vecenv* v) { return v->launches; }
 
+int ut_vecenv_enable_phase_timing(ut_vecenv* v, int on) {
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  if (on && !v->B.phase_cycles) {
+    unsigned long long* p;
+    int rc;
+    if ((rc = v->alloc(&p, (size_t)(v->n_envs * kPhaseCount)))) return rc;
+    UT_CUDA(cudaMemset(p, 0, sizeof(unsigned long long) * v->n_envs * kPhaseCount));
+    v->B.phase_cycles = p;
+  } else if (!on) {
+    v->B.phase_cycles = nullptr;  // buffer stays owned by the handle
+  }
+  return UT_OK;
+}
+
+int ut_vecenv_phase_cycles(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset) {
+  for (int k = 0; k < UT_N_PHASES; ++k) out[k] = 0;
+  if (!v->B.phase_cycles) return UT_OK;
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  std::vector<unsigned long long> h((size_t)(v->n_envs * kPhaseCount));
+  UT_CUDA(cudaMemcpy(h.data(), v->B.phase_cycles, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+  for (int64_t e = 0; e < v->n_envs; ++e)
+    for (int k = 0; k < kPhaseCount; ++k) out[k] += h[(size_t)(e * kPhaseCount + k)];
+  if (reset) UT_CUDA(cudaMemset(v->B.phase_cycles, 0, sizeof(unsigned long long) * h.size()));
+  return UT_OK;
+}
+
 // Environment::serialize_state (env.cpp:550-593)
 int ut_env_serialize(ut_vecenv* v, int64_t e, double* blob, size_t cap, size_t* len) {
   if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "serialize: env %lld out of range", (long long)e);
@@ -611,7 +640,7 @@ int ut_env_serialize(ut_vecenv* v, int64_t e, double* blob, size_t cap, size_t* 
       for (int fl = 0; fl < I_NFIELD; ++fl) blob[i++] = info[fl * AA + a * A + j];
     for (int t = 0; t < T; ++t) {
       const int si = a * T + t;
-      for (int fl = 0; fl < K_NFIELD; ++fl) blob[i++] = trk[fl * AT + si];
+      for (int fl = 0; fl < K_NBLOB; ++fl) blob[i++] = trk[fl * AT + si];
       for (int k = 0; k < 5; ++k) {
         std::memcpy(blob + i, f[k].data() + (size_t)si * P, sizeof(double) * P);
         i += (size_t)P;
@@ -668,7 +697,7 @@ int ut_env_deserialize(ut_vecenv* v, int64_t e, const double* blob, size_t len) 
       }
     for (int t = 0; t < T; ++t) {
       const int si = a * T + t;
-      for (int fl = 0; fl < K_NFIELD; ++fl) {
+      for (int fl = 0; fl < K_NBLOB; ++fl) {
         const double x = blob[i++];
         double& dst = trk[fl * AT + si];
         dst = fl == K_AGE ? as_int(x)
@@ -676,6 +705,7 @@ int ut_env_deserialize(ut_vecenv* v, int64_t e, const double* blob, size_t len) 
               : fl == K_POS ? (double)(uint64_t)x
                             : x;
       }
+      trk[K_ESSOK * AT + si] = 0.0;  // injected weights have not been vetted
       for (int k = 0; k < 5; ++k) {
         std::memcpy(f[k].data() + (size_t)si * P, blob + i, sizeof(double) * P);
         i += (size_t)P;
@@ -759,6 +789,11 @@ __global__ void derive_key_kernel(uint64_t a, uint64_t b, uint64_t c, uint64_t d
 #include "ut_debug.h"
 
 extern "C" {
+int ut_debug_set_knobs(ut_vecenv* v, int force_exact, int64_t trace_env) {
+  v->B.force_exact = force_exact;
+  v->B.trace_env = trace_env;
+  return UT_OK;
+}
 int ut_debug_abi_sizes(int64_t out[4]) {
   out[0] = sizeof(ut_env_config);
   out[1] = sizeof(ut_buffers);

@@ -3,12 +3,18 @@
 // One CTA steps one environment end to end (north_star "one fused kernel per
 // step"): the env record is staged in shared memory, one thread runs the serial
 // env-stream prologue (Appendix A order: targets, agents, pings, comm drops),
-// then the whole CTA runs every particle set of the env -- predict, the ordered
-// range updates, ESS + systematic resample, estimate -- with the set held in
-// registers (PPT particles per thread, particle k = tid + j * blockDim.x, so all
-// HBM traffic is coalesced 8-byte lanes and each set is read once and written
-// once), then the epilogue (reward, done, tokens, masks) and, for finished envs,
-// the auto-reset (spawn + particle re-init) before the record is written back.
+// then the whole CTA runs every particle set of the env with the set held in
+// registers -- PPT consecutive particles per thread (128-bit coalesced loads and
+// stores, each set read once and written once per step) -- then the epilogue
+// (reward, done, tokens, masks) and, for finished envs, the auto-reset (spawn +
+// particle re-init) before the record is written back.
+//
+// Per set the work is: predict (Philox words generated one set ahead into a
+// double-buffered smem area, correctly rounded fp32 Box-Muller), ONE merged pass
+// for all of this step's range updates (per-stage maxima kept so the reference's
+// sequential semantics hold; the exact sequential path runs whenever an
+// intermediate underflow could matter), ESS from the same reduction, systematic
+// resample (scan + search), estimate in one shifted reduction.
 #pragma once
 #include "ut_device.cuh"
 
@@ -16,43 +22,55 @@ namespace ut {
 
 enum StepMode : int { MODE_EXTERNAL = -1, MODE_RANDOM = 0, MODE_SCRIPTED = 1 };
 enum DevStatus : int { ST_OK = 0, ST_SPAWN_INFEASIBLE = 2 };
+constexpr int kMaxMerged = 8;   // merged update handles up to 8 measurements per set
+constexpr int kMeasStride = 8;  // ox, oy, r2, sigma, 1/sigma (+pad)
+constexpr double kMergeFloor = 0x1p-860;  // see the merged-update argument in step_set
 
 // ------------------------------------------------------------ smem carve ---
 struct Smem {
+  double2* tab_log;    // [128]
+  double2* tab_sc;     // [64]
   double* rec;
-  double* meas;  // [A*T][4] ox, oy, r2, sigma
-  double* red;   // 160: BlockReducer (2 x 64) + resample warp offsets (32)
-  double* bc;    // 16 broadcast slots
-  double* qxy;   // [2 * R] spawn scratch
-  int* act;      // [A]
-  uint8_t* present;
-  uint8_t* fresh;
-  uint8_t* link;
-  unsigned char* uni;  // union buffer: Philox words | resample cum + staging
+  double* meas;        // [A*T][kMeasStride]
+  double* red;         // kRedDoubles: BlockReducer buffers + scan warp sums
+  double* bc;          // 16 broadcast slots
+  double* qxy;         // [2 * R] spawn scratch
+  int* act;            // [A]
+  uint8_t* present;    // [A*T]
+  uint8_t* link;       // [A*A]
+  uint8_t* mcount;     // [A*T] measurements applied to each set this step
+  uint8_t* mlist;      // [A*T][A] their meas indices in application order
+  uint32_t* words[2];  // Philox words, double buffered: 4P + 2 (+ 8 slack)
+  double* cum;         // [P] resample scan
+  double* st;          // [4P] resample staging
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline size_t uni_bytes(int P) {
-  const size_t a = (size_t)40 * P;                  // resample: cum + 4 staged fields
-  const size_t b = (size_t)16 * (2 * (size_t)P + 2);  // re-init: 8P words (+ partial blocks)
-  const size_t c = (size_t)16 * ((size_t)P + 2);      // predict: 4P words
-  size_t m = a > b ? a : b;
-  m = m > c ? m : c;
-  return align16(m + 64);
+__host__ __device__ inline size_t words_bytes(int P) {
+  // predict uses 4P words + 2 for the resample u0; one extra block covers a
+  // misaligned start. (Re-init's 8P words use the resample area instead.)
+  return align16((size_t)4 * (4 * (size_t)P + 2 + 8));
+}
+__host__ __device__ inline size_t resample_bytes(int P) {
+  const size_t a = sizeof(double) * 5 * (size_t)P;  // cum + 4 staged fields
+  const size_t b = (size_t)4 * (8 * (size_t)P + 8);  // re-init words
+  return align16(a > b ? a : b);
 }
 
 __host__ __device__ inline size_t smem_bytes(int rec_words, int A, int T, int P) {
   const int R = A + T;
   size_t s = 0;
+  s += sizeof(double2) * (128 + 64);
   s += align16(sizeof(double) * rec_words);
-  s += align16(sizeof(double) * 4 * A * T);
-  s += align16(sizeof(double) * 160);
+  s += align16(sizeof(double) * kMeasStride * A * T);
+  s += align16(sizeof(double) * kRedDoubles);
   s += align16(sizeof(double) * 16);
   s += align16(sizeof(double) * 2 * R);
   s += align16(sizeof(int) * A);
-  s += align16(A * T) * 2 + align16(A * A);
-  s += uni_bytes(P);
+  s += align16(A * T) + align16(A * A) + align16(A * T) + align16(A * T * A);
+  s += 2 * words_bytes(P);
+  s += resample_bytes(P);
   return s;
 }
 
@@ -60,12 +78,16 @@ __device__ inline Smem carve(unsigned char* base, int rec_words, int A, int T, i
   Smem S;
   const int R = A + T;
   size_t o = 0;
+  S.tab_log = (double2*)(base + o);
+  o += sizeof(double2) * 128;
+  S.tab_sc = (double2*)(base + o);
+  o += sizeof(double2) * 64;
   S.rec = (double*)(base + o);
   o += align16(sizeof(double) * rec_words);
   S.meas = (double*)(base + o);
-  o += align16(sizeof(double) * 4 * A * T);
+  o += align16(sizeof(double) * kMeasStride * A * T);
   S.red = (double*)(base + o);
-  o += align16(sizeof(double) * 160);
+  o += align16(sizeof(double) * kRedDoubles);
   S.bc = (double*)(base + o);
   o += align16(sizeof(double) * 16);
   S.qxy = (double*)(base + o);
@@ -74,11 +96,18 @@ __device__ inline Smem carve(unsigned char* base, int rec_words, int A, int T, i
   o += align16(sizeof(int) * A);
   S.present = base + o;
   o += align16(A * T);
-  S.fresh = base + o;
-  o += align16(A * T);
   S.link = base + o;
   o += align16(A * A);
-  S.uni = base + o;
+  S.mcount = base + o;
+  o += align16(A * T);
+  S.mlist = base + o;
+  o += align16(A * T * A);
+  S.words[0] = (uint32_t*)(base + o);
+  o += words_bytes(P);
+  S.words[1] = (uint32_t*)(base + o);
+  o += words_bytes(P);
+  S.cum = (double*)(base + o);
+  S.st = S.cum + P;
   return S;
 }
 
@@ -92,10 +121,15 @@ __device__ __forceinline__ int64_t set_off(const DevBatch& B, int64_t e) {
   return B.set_offset ? B.set_offset[e] : e * (int64_t)(B.cfgs[0].A * B.cfgs[0].T);
 }
 
+__device__ __forceinline__ void load_tables(const Smem& S) {
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) S.tab_log[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) S.tab_sc[i] = make_double2(kSinCosTab[2 * i], kSinCosTab[2 * i + 1]);
+}
+
 // --------------------------------------------------- serial env prologue ---
 // Environment::scripted_action (env.cpp:511-543) for every agent, on the
 // pre-step state (VecEnv::step_policy computes all actions first, vecenv.cpp:123-124).
-__device__ void scripted_actions(const DevConfig& c, const double* rec, int* act) {
+__device__ __noinline__ void scripted_actions(const DevConfig& c, const double* rec, int* act) {
   const int A = c.A, T = c.T, AT = A * T;
   const double* ag = rec + c.o_agent;
   const double* trk = rec + c.o_track;
@@ -131,8 +165,9 @@ __device__ void scripted_actions(const DevConfig& c, const double* rec, int* act
 }
 
 // Actions + move_targets + move_agents + measure_ranges + comm decisions, in
-// the reference's env-stream draw order. Thread 0 only.
-__device__ void env_prologue(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t e, int64_t gi,
+// the reference's env-stream draw order, then the per-set
+// measurement schedule. Thread 0 only.
+__device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t e, int64_t gi,
                              int mode) {
   const int A = c.A, T = c.T;
   double* rec = S.rec;
@@ -209,18 +244,18 @@ __device__ void env_prologue(const DevConfig& c, const DevBatch& B, const Smem& 
       r3 = r3 < 0.0 ? 0.0 : r3;
       const double dd = tz - az;
       const double sq = r3 * r3 - dd * dd;  // slant_to_horizontal (tracking.cpp:9-14)
-      double* m = S.meas + 4 * idx;
+      double* m = S.meas + kMeasStride * idx;
       m[0] = ax;
       m[1] = ay;
       m[2] = sq <= 0.0 ? 0.0 : sqrt(sq);
       m[3] = c.sigma_meas;
+      m[4] = 1.0 / c.sigma_meas;
       S.present[idx] = 1;
       detected = true;
     }
     miss[t] = detected ? 0.0 : miss[t] + 1.0;
   }
-  // exchange_comms decisions (env.cpp:365-383); the fused filter updates run in
-  // the per-set phase in the same (sender-ascending) order.
+  // exchange_comms decisions (env.cpp:365-383)
   for (int i = 0; i < AA; ++i) info[I_AGE * AA + i] += 1.0;
   for (int r = 0; r < A; ++r)
     for (int s = 0; s < A; ++s) {
@@ -238,6 +273,17 @@ __device__ void env_prologue(const DevConfig& c, const DevBatch& B, const Smem& 
       info[I_VALID * AA + k] = 1.0;
       S.link[k] = 1;
     }
+  // per-set update schedule: own ping first (env.cpp:356-360), then the fused
+  // senders in ascending order (env.cpp:370-392)
+  for (int a = 0; a < A; ++a)
+    for (int t = 0; t < T; ++t) {
+      const int si = a * T + t;
+      int n = 0;
+      if (S.present[si]) S.mlist[si * A + n++] = (uint8_t)si;
+      for (int s = 0; s < A; ++s)
+        if (s != a && S.link[a * A + s] && S.present[s * T + t]) S.mlist[si * A + n++] = (uint8_t)(s * T + t);
+      S.mcount[si] = (uint8_t)n;
+    }
   rec[R_ENV_POS] = (double)rng.pos;
   rec[R_ENV_HAVE_SPARE] = rng.have_spare ? 1.0 : 0.0;
   rec[R_ENV_SPARE] = rng.spare;
@@ -249,27 +295,101 @@ struct SetRegs {
   double px[PPT], py[PPT], vx[PPT], vy[PPT], w[PPT];
 };
 
-// Block-wide generation of the u32 words [pos, pos + n_words) into smem;
-// word(pos + m) == words[(pos & 3) + m]. One Philox block per thread-iteration.
+// Words [pos, pos + n_words) of one stream into smem (no barrier):
+// word(pos + m) == words[(pos & 3) + m].
 __device__ __forceinline__ void gen_words(uint32_t* words, uint64_t key, uint64_t stream, uint64_t pos,
                                           uint64_t n_words) {
   const uint64_t b0 = pos >> 2;
   const int nb = (int)(((pos + n_words - 1) >> 2) - b0 + 1);
   uint4* w4 = reinterpret_cast<uint4*>(words);
   for (int i = threadIdx.x; i < nb; i += blockDim.x) w4[i] = philox(key, stream, b0 + (uint64_t)i);
-  __syncthreads();
 }
 
-// pf::update with one measurement (tracking.cpp:119-143).
+// 4 consecutive words starting at idx (idx % 4 uniform across the warp).
+__device__ __forceinline__ uint4 lds_words4(const uint32_t* w, int idx) {
+  if ((idx & 3) == 0) return *reinterpret_cast<const uint4*>(w + idx);
+  if ((idx & 1) == 0) {
+    const uint2 a = *reinterpret_cast<const uint2*>(w + idx);
+    const uint2 b = *reinterpret_cast<const uint2*>(w + idx + 2);
+    return make_uint4(a.x, a.y, b.x, b.y);
+  }
+  return make_uint4(w[idx], w[idx + 1], w[idx + 2], w[idx + 3]);
+}
+
 template <int PPT>
-__device__ __forceinline__ void pf_update(SetRegs<PPT>& s, const double* m, int P, BlockReducer& R) {
+__device__ __forceinline__ void load_set(SetRegs<PPT>& s, const DevBatch& B, size_t base, int k0, int P) {
+  if (PPT == 4 && k0 + 4 <= P && (P & 3) == 0) {
+    const double2* px = reinterpret_cast<const double2*>(B.px + base + k0);
+    const double2* py = reinterpret_cast<const double2*>(B.py + base + k0);
+    const double2* vx = reinterpret_cast<const double2*>(B.vx + base + k0);
+    const double2* vy = reinterpret_cast<const double2*>(B.vy + base + k0);
+    const double2* w = reinterpret_cast<const double2*>(B.w + base + k0);
+    double2 t[10] = {px[0], px[1], py[0], py[1], vx[0], vx[1], vy[0], vy[1], w[0], w[1]};
+    s.px[0] = t[0].x, s.px[1] = t[0].y, s.px[2] = t[1].x, s.px[3] = t[1].y;
+    s.py[0] = t[2].x, s.py[1] = t[2].y, s.py[2] = t[3].x, s.py[3] = t[3].y;
+    s.vx[0] = t[4].x, s.vx[1] = t[4].y, s.vx[2] = t[5].x, s.vx[3] = t[5].y;
+    s.vy[0] = t[6].x, s.vy[1] = t[6].y, s.vy[2] = t[7].x, s.vy[3] = t[7].y;
+    s.w[0] = t[8].x, s.w[1] = t[8].y, s.w[2] = t[9].x, s.w[3] = t[9].y;
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int k = k0 + j;
+    if (k < P) {
+      s.px[j] = B.px[base + k];
+      s.py[j] = B.py[base + k];
+      s.vx[j] = B.vx[base + k];
+      s.vy[j] = B.vy[base + k];
+      s.w[j] = B.w[base + k];
+    } else {
+      s.px[j] = s.py[j] = s.vx[j] = s.vy[j] = s.w[j] = 0.0;
+    }
+  }
+}
+
+template <int PPT>
+__device__ __forceinline__ void store_set(const SetRegs<PPT>& s, const DevBatch& B, size_t base, int k0, int P) {
+  if (PPT == 4 && k0 + 4 <= P && (P & 3) == 0) {
+    double2* px = reinterpret_cast<double2*>(B.px + base + k0);
+    double2* py = reinterpret_cast<double2*>(B.py + base + k0);
+    double2* vx = reinterpret_cast<double2*>(B.vx + base + k0);
+    double2* vy = reinterpret_cast<double2*>(B.vy + base + k0);
+    double2* w = reinterpret_cast<double2*>(B.w + base + k0);
+    px[0] = make_double2(s.px[0], s.px[1]);
+    px[1] = make_double2(s.px[2], s.px[3]);
+    py[0] = make_double2(s.py[0], s.py[1]);
+    py[1] = make_double2(s.py[2], s.py[3]);
+    vx[0] = make_double2(s.vx[0], s.vx[1]);
+    vx[1] = make_double2(s.vx[2], s.vx[3]);
+    vy[0] = make_double2(s.vy[0], s.vy[1]);
+    vy[1] = make_double2(s.vy[2], s.vy[3]);
+    w[0] = make_double2(s.w[0], s.w[1]);
+    w[1] = make_double2(s.w[2], s.w[3]);
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int k = k0 + j;
+    if (k < P) {
+      B.px[base + k] = s.px[j];
+      B.py[base + k] = s.py[j];
+      B.vx[base + k] = s.vx[j];
+      B.vy[base + k] = s.vy[j];
+      B.w[base + k] = s.w[j];
+    }
+  }
+}
+
+// pf::update with one measurement (tracking.cpp:119-143) -- the exact
+// sequential path.
+template <int PPT>
+__device__ __noinline__ void pf_update_seq(SetRegs<PPT>& s, const double* m, int k0, int P, BlockReducer& R) {
   const double ox = m[0], oy = m[1], r2 = m[2], sig = m[3];
   double ll[PPT];
   double mx = -CUDART_INF;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    const int k = threadIdx.x + j * blockDim.x;
-    if (k < P) {
+    if (k0 + j < P) {
       const double dx = s.px[j] - ox, dy = s.py[j] - oy;
       const double d = sqrt(dx * dx + dy * dy);
       const double q = (d - r2) / sig;
@@ -284,8 +404,7 @@ __device__ __forceinline__ void pf_update(SetRegs<PPT>& s, const double* m, int 
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const int k = threadIdx.x + j * blockDim.x;
-      if (k < P) {
+      if (k0 + j < P) {
         s.w[j] = s.w[j] * exp(ll[j] - shift);
         acc = acc + s.w[j];
       }
@@ -299,73 +418,67 @@ __device__ __forceinline__ void pf_update(SetRegs<PPT>& s, const double* m, int 
   }
   const double inv = 1.0 / (double)P;
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = threadIdx.x + j * blockDim.x;
-    s.w[j] = k < P ? inv : 0.0;
-  }
+  for (int j = 0; j < PPT; ++j) s.w[j] = k0 + j < P ? inv : 0.0;
 }
 
-// pf::estimate (tracking.cpp:180-188) -> (mean x, mean y, spread)
+// pf::estimate (tracking.cpp:180-188) in ONE reduction: moments about the set's
+// previous estimate (cx, cy), mean = c + sum w (p - c), spread^2 = second moment
+// minus the squared shift; exact second pass when that subtraction could lose
+// more than ~1e-11 relative.
 template <int PPT>
-__device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int P, BlockReducer& R) {
-  double sx = 0.0, sy = 0.0;
+__device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, int P, double cx, double cy,
+                                               BlockReducer& R) {
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    const int k = threadIdx.x + j * blockDim.x;
-    if (k < P) {
-      sx = sx + s.w[j] * s.px[j];
-      sy = sy + s.w[j] * s.py[j];
+    if (k0 + j < P) {
+      const double dx = s.px[j] - cx, dy = s.py[j] - cy;
+      a0 = a0 + s.w[j] * dx;
+      a1 = a1 + s.w[j] * dy;
+      a2 = a2 + s.w[j] * (dx * dx + dy * dy);
     }
   }
-  const double2 m = R.sum2(sx, sy);
+  const double3 m = R.sum3(a0, a1, a2);
+  const double mx = cx + m.x, my = cy + m.y;
+  const double shift2 = m.x * m.x + m.y * m.y;
+  const double var = m.z - shift2;
+  if (var > 1e-5 * shift2) return make_double3(mx, my, sqrt(var));
   double acc = 0.0;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    const int k = threadIdx.x + j * blockDim.x;
-    if (k < P) {
-      const double dx = s.px[j] - m.x, dy = s.py[j] - m.y;
+    if (k0 + j < P) {
+      const double dx = s.px[j] - mx, dy = s.py[j] - my;
       acc = acc + s.w[j] * (dx * dx + dy * dy);
     }
   }
-  const double v = R.sum(acc);
-  return make_double3(m.x, m.y, sqrt(v));
+  return make_double3(mx, my, sqrt(R.sum(acc)));
 }
 
 // pf::resample (tracking.cpp:147-170): inclusive scan of w in index order, then
-// each output j takes the first particle whose cumulative weight reaches
-// (j + u0) / n (clamped to n - 1) -- the reference's monotone two-pointer walk.
+// output j takes the first particle whose cumulative weight reaches (j + u0)/n,
+// clamped to n - 1 (the reference's monotone two-pointer walk): a binary search
+// for the thread's first output, a forward walk for the rest.
 template <int PPT>
-__device__ void pf_resample(SetRegs<PPT>& s, int P, double u0, unsigned char* uni, double* red) {
+__device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Smem& S) {
   const int tid = threadIdx.x, NT = blockDim.x;
-  double* cum = reinterpret_cast<double*>(uni);
-  double* st = cum + P;
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = tid + j * NT;
-    if (k < P) {
-      cum[k] = s.w[j];
-      st[k] = s.px[j];
-      st[P + k] = s.py[j];
-      st[2 * P + k] = s.vx[j];
-      st[3 * P + k] = s.vy[j];
-    }
-  }
-  __syncthreads();
-  // contiguous chunk per thread
-  const int C = (P + NT - 1) / NT;  // <= PPT
-  const int lo = tid * C;
-  const int hi = min(lo + C, P);
+  double* cum = S.cum;
+  double* st = S.st;
+  double* wsum = S.red + 2 * kRedSlots;
   double loc[PPT];
   double run = 0.0;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
-    if (q < C && lo + q < hi) {
-      run = (q == 0) ? cum[lo] : run + cum[lo + q];
-      loc[q] = run;
+    const int k = k0 + q;
+    if (k < P) {
+      st[k] = s.px[q];
+      st[P + k] = s.py[q];
+      st[2 * P + k] = s.vx[q];
+      st[3 * P + k] = s.vy[q];
+      run = q == 0 ? s.w[q] : run + s.w[q];
     }
+    loc[q] = run;
   }
-  // exclusive prefix of the thread totals: warp scan + sequential warp offsets
-  const int lane = tid & 31, warp = tid >> 5, nw = NT >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   double incl = run;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -374,7 +487,6 @@ __device__ void pf_resample(SetRegs<PPT>& s, int P, double u0, unsigned char* un
   }
   double excl = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) excl = 0.0;
-  double* wsum = red;  // 32 slots (the reducer's buffers are idle here)
   if (lane == 31) wsum[warp] = incl;
   __syncthreads();
   double woff = 0.0;
@@ -382,60 +494,78 @@ __device__ void pf_resample(SetRegs<PPT>& s, int P, double u0, unsigned char* un
   const double base = woff + excl;
 #pragma unroll
   for (int q = 0; q < PPT; ++q)
-    if (q < C && lo + q < hi) cum[lo + q] = (lo == 0 && q == 0) ? loc[0] : base + loc[q];
-  (void)nw;
+    if (k0 + q < P) cum[k0 + q] = base + loc[q];
+  (void)NT;
   __syncthreads();
   const double inv_n = 1.0 / (double)P;
+  if (k0 < P) {
+    const double u = ((double)k0 + u0) * inv_n;
+    int a = 0, b = P - 1;
+    while (a < b) {
+      const int mid = (a + b) >> 1;
+      if (cum[mid] < u)
+        a = mid + 1;
+      else
+        b = mid;
+    }
+    int i = a;
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int m = tid + j * NT;
-    if (m < P) {
-      const double u = ((double)m + u0) * inv_n;
-      int a = 0, b = P - 1;
-      while (a < b) {
-        const int mid = (a + b) >> 1;
-        if (cum[mid] < u)
-          a = mid + 1;
-        else
-          b = mid;
+    for (int q = 0; q < PPT; ++q) {
+      const int j = k0 + q;
+      if (j < P) {
+        const double uj = ((double)j + u0) * inv_n;
+        // lower_bound over [i, P-1]: usually i or i+1; otherwise a binary search
+        // (a plain forward walk diverges over runs of zero-weight particles)
+        if (i < P - 1 && cum[i] < uj) {
+          ++i;
+          if (i < P - 1 && cum[i] < uj) {
+            int lo = i + 1, hi = P - 1;
+            while (lo < hi) {
+              const int mid = (lo + hi) >> 1;
+              if (cum[mid] < uj)
+                lo = mid + 1;
+              else
+                hi = mid;
+            }
+            i = lo;
+          }
+        }
+        s.px[q] = st[i];
+        s.py[q] = st[P + i];
+        s.vx[q] = st[2 * P + i];
+        s.vy[q] = st[3 * P + i];
+        s.w[q] = inv_n;
       }
-      s.px[j] = st[a];
-      s.py[j] = st[P + a];
-      s.vx[j] = st[2 * P + a];
-      s.vy[j] = st[3 * P + a];
-      s.w[j] = inv_n;
     }
   }
   __syncthreads();
 }
 
-// filter_step (env.cpp:349-363) + the fused comm updates (env.cpp:385-392) +
-// the finalize pass (env.cpp:397-409) for ONE set, fully in registers.
+// filter_step (env.cpp:349-363) + fused comm updates (env.cpp:385-392) +
+// finalize (env.cpp:397-409) for ONE set. `wb` is this set's words buffer; the
+// next set's words (if any) are generated into the other buffer on the way.
 template <int PPT>
 __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int64_t gi,
-                         int64_t gset, int a, int t, double* stat_upd, double* stat_res) {
-  const int P = c.P, tid = threadIdx.x, NT = blockDim.x, A = c.A, T = c.T, AT = A * T;
+                         int64_t gset, int a, int t, int wb, double* stat) {
+  const int P = c.P, tid = threadIdx.x, A = c.A, T = c.T, AT = A * T;
   const int si = a * T + t;
+  const int k0 = tid * PPT;
   double* trk = S.rec + c.o_track;
   uint64_t pos = (uint64_t)trk[K_POS * AT + si];
   const double ms = trk[K_MAXSPEED * AT + si];
   const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)si);
-  const uint64_t stream = (uint64_t)si;
   const size_t base = (size_t)gset * P;
+  const uint32_t* words = S.words[wb];
+  const int off = (int)(pos & 3);
 
   SetRegs<PPT> s;
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = tid + j * NT;
-    if (k < P) {
-      s.px[j] = B.px[base + k];
-      s.py[j] = B.py[base + k];
-      s.vx[j] = B.vx[base + k];
-      s.vy[j] = B.vy[base + k];
-      s.w[j] = B.w[base + k];
-    } else {
-      s.px[j] = s.py[j] = s.vx[j] = s.vy[j] = s.w[j] = 0.0;
-    }
+  load_set<PPT>(s, B, base, k0, P);
+
+  // Next set's words into the other buffer (made visible by this set's barriers).
+  if (si + 1 < AT) {
+    const uint64_t npos = (uint64_t)trk[K_POS * AT + si + 1];
+    gen_words(S.words[wb ^ 1], derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)(si + 1)), (uint64_t)(si + 1),
+              npos, (c.noise_on ? 4ull * (uint64_t)P : 0ull) + 2ull);
   }
 
   // ---- pf::predict (tracking.cpp:94-117)
@@ -445,35 +575,43 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     s.py[j] = s.py[j] + s.vy[j] * c.dt;
   }
   if (c.noise_on) {
-    uint32_t* words = reinterpret_cast<uint32_t*>(S.uni);
-    gen_words(words, key, stream, pos, 4ull * (uint64_t)P);
-    const int off = (int)(pos & 3);
     const float two_pi_f = 2.0f * 3.14159265358979323846f;
+    // fill_normals: pair i uses u1 = word(pos + i), u2 = word(pos + 2P + i);
+    // particle k takes cos of pairs k and P+k, sin of pairs k and P+k.
+    uint4 W[4];
+    if (PPT == 4 && k0 + 4 <= P) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) W[q] = lds_words4(words, off + q * P + k0);
+    }
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const int k = tid + j * NT;
+      const int k = k0 + j;
       if (k < P) {
-        // fill_normals (tracking.cpp:24-37): pair i uses u1 = word(c+i), u2 = word(c+2P+i)
-        const uint32_t w1a = words[off + k], w1b = words[off + P + k];
-        const uint32_t w2a = words[off + 2 * P + k], w2b = words[off + 3 * P + k];
-        const float u1a = (float)((w1a >> 8) + 1u) * 0x1.0p-24f;
-        const float u1b = (float)((w1b >> 8) + 1u) * 0x1.0p-24f;
-        const float u2a = (float)(w2a >> 8) * 0x1.0p-24f;
-        const float u2b = (float)(w2b >> 8) * 0x1.0p-24f;
-        const float ra = __fsqrt_rn(-2.0f * cr_logf(u1a));
-        const float rb = __fsqrt_rn(-2.0f * cr_logf(u1b));
-        float sa, ca, sb, cb;
-        cr_sincosf(__fmul_rn(two_pi_f, u2a), &sa, &ca);
-        cr_sincosf(__fmul_rn(two_pi_f, u2b), &sb, &cb);
-        const float zpx = __fmul_rn(ra, ca), zvx = __fmul_rn(ra, sa);  // out[k], out[2P+k]
-        const float zpy = __fmul_rn(rb, cb), zvy = __fmul_rn(rb, sb);  // out[P+k], out[3P+k]
+        uint32_t w1a, w1b, w2a, w2b;
+        if (PPT == 4 && k0 + 4 <= P) {
+          w1a = lane_of(W[0], j);
+          w1b = lane_of(W[1], j);
+          w2a = lane_of(W[2], j);
+          w2b = lane_of(W[3], j);
+        } else {
+          w1a = words[off + k];
+          w1b = words[off + P + k];
+          w2a = words[off + 2 * P + k];
+          w2b = words[off + 3 * P + k];
+        }
+        float zpx, zvx, zpy, zvy;  // out[k], out[2P+k] / out[P+k], out[3P+k]
+        bool ok = box_muller_fast(w1a, w2a, S.tab_log, S.tab_sc, zpx, zvx);
+        ok &= box_muller_fast(w1b, w2b, S.tab_log, S.tab_sc, zpy, zvy);
+        if (!ok) {  // an uncertain rounding (p ~ 1e-4 per particle): exact fp64 libm path
+          box_muller_slow(w1a, w2a, zpx, zvx);
+          box_muller_slow(w1b, w2b, zpy, zvy);
+        }
         s.px[j] = s.px[j] + c.pn * (double)zpx;
         s.py[j] = s.py[j] + c.pn * (double)zpy;
         s.vx[j] = s.vx[j] + c.vn * (double)zvx;
         s.vy[j] = s.vy[j] + c.vn * (double)zvy;
       }
     }
-    pos += 4ull * (uint64_t)P;
   }
   if (ms > 0.0) {
 #pragma unroll
@@ -484,51 +622,127 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       s.vy[j] = s.vy[j] * f;
     }
   }
+  const int u0_idx = off + (c.noise_on ? 4 * P : 0);  // resample draw follows predict's 4P
+  if (c.noise_on) pos += 4ull * (uint64_t)P;
 
-  // ---- own update, then fused updates in sender order (env.cpp:356-360, 385-392)
-  int n_upd = 0;
-  if (S.present[si]) {
-    pf_update<PPT>(s, S.meas + 4 * si, P, R);
-    ++n_upd;
+  // ---- range updates: own ping, then fused senders (env.cpp:356-360, 385-392)
+  const int nm = S.mcount[si];
+  const uint8_t* ml = S.mlist + si * A;
+  bool have_ess = false;
+  double ess = 0.0;
+  bool exact = nm > kMaxMerged || B.force_exact;
+  if (nm > 0 && !exact) {
+    // Merged pass. With L_i = sum_j ll_ij and s_j = max_i ll_ij, the sequential
+    // reference computes e_i / sum(e) with e_i = w_i exp(L_i - sum_j s_j), up to
+    // rounding, unless an intermediate product underflows. Every intermediate
+    // product of particle i is >= e_i (each ll - s <= 0, each stage sum <= 1).
+    // Particles with e_i < 2^-60 max(e) are invisible in every fp64 sum either
+    // way; all others have products >= 2^-60 max(e) >= 2^-920 (normal) when
+    // max(e) >= 2^-860, and no stage can degenerate. So under that check the
+    // merged result equals the sequential one to rounding; otherwise (or with a
+    // non-finite shift) the exact sequential path runs.
+    double L[PPT];
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) L[q] = 0.0;
+    double* mb = R.buf();  // per-stage warp maxima, [stage * 32 + warp]
+    const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+#pragma unroll 1
+    for (int j = 0; j < nm; ++j) {
+      const double* m = S.meas + kMeasStride * ml[j];
+      const double ox = m[0], oy = m[1], r2 = m[2], sig = m[3], rsig = m[4];
+      double mj = -CUDART_INF;
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        if (k0 + q < P) {
+          const double dx = s.px[q] - ox, dy = s.py[q] - oy;
+          const double d = sqrt(dx * dx + dy * dy);
+          const double qv = div_rcp(d - r2, sig, rsig);
+          const double ll = 0.0 - 0.5 * (qv * qv);
+          L[q] = L[q] + ll;
+          mj = ll > mj ? ll : mj;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, mj, o);
+        mj = u > mj ? u : mj;
+      }
+      if (lane == 0) mb[j * 32 + warp] = mj;
+    }
+    __syncthreads();
+    double shift = 0.0;  // sum_j s_j, in stage order
+#pragma unroll 1
+    for (int j = 0; j < nm; ++j) {
+      double sj = lane < nw ? mb[j * 32 + lane] : -CUDART_INF;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, sj, o);
+        sj = u > sj ? u : sj;
+      }
+      shift = j == 0 ? sj : shift + sj;
+    }
+    if (!isfinite(shift)) {
+      exact = true;
+    } else {
+      double e[PPT], ls = 0.0, lq = 0.0, lm = 0.0;
+#pragma unroll
+      for (int q = 0; q < PPT; ++q) {
+        e[q] = 0.0;
+        if (k0 + q < P) {
+          e[q] = s.w[q] * exp(L[q] - shift);
+          ls = ls + e[q];
+          lq = lq + e[q] * e[q];
+          lm = e[q] > lm ? e[q] : lm;
+        }
+      }
+      const double3 r = R.sum2_max(ls, lq, lm);
+      if (isfinite(r.x) && r.x > 0.0 && r.z >= kMergeFloor) {
+        const double rcp = 1.0 / r.x;
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) s.w[q] = div_rcp(e[q], r.x, rcp);
+        // ESS = sum^2 / sum(e^2) unless the squares may have underflowed
+        if (r.z >= 0x1p-200) {
+          ess = (r.x * r.x) / r.y;
+          have_ess = true;
+        }
+      } else {
+        exact = true;
+      }
+    }
+    if (exact && tid == 0) stat[2] += 1.0;
   }
-  bool fused = false;
-  for (int snd = 0; snd < A; ++snd) {
-    if (snd == a || !S.link[a * A + snd] || !S.present[snd * T + t]) continue;
-    pf_update<PPT>(s, S.meas + 4 * (snd * T + t), P, R);
-    ++n_upd;
-    fused = true;
+  if (exact) {
+    for (int j = 0; j < nm; ++j) pf_update_seq<PPT>(s, S.meas + kMeasStride * ml[j], k0, P, R);
   }
-  const bool fresh = S.present[si] || fused;
+  const bool fresh = nm > 0;
 
   // ---- pf::maybe_resample (tracking.cpp:172-178)
-  double w2 = 0.0;
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) w2 = w2 + s.w[j] * s.w[j];
-  const double ess = 1.0 / R.sum(w2);
   bool resampled = false;
-  if (ess < (double)P / 2.0) {
-    // u0 = uniform() from the set's stream (tracking.cpp:149)
-    const uint64_t lo = word_at(key, stream, pos), hi = word_at(key, stream, pos + 1);
-    const double u0 = (double)(((hi << 32) | lo) >> 11) * 0x1.0p-53;
-    pos += 2;
-    pf_resample<PPT>(s, P, u0, S.uni, R.red + 128);
-    resampled = true;
-  }
-
-  // ---- estimate (env.cpp:403-407)
-  const double3 est = pf_estimate<PPT>(s, P, R);
-
+  const bool ess_known_ok = nm == 0 && trk[K_ESSOK * AT + si] != 0.0;
+  if (!ess_known_ok) {
+    if (!have_ess) {
+      double w2 = 0.0;
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = tid + j * NT;
-    if (k < P) {
-      B.px[base + k] = s.px[j];
-      B.py[base + k] = s.py[j];
-      B.vx[base + k] = s.vx[j];
-      B.vy[base + k] = s.vy[j];
-      B.w[base + k] = s.w[j];
+      for (int q = 0; q < PPT; ++q) w2 = w2 + s.w[q] * s.w[q];
+      ess = 1.0 / R.sum(w2);
+    }
+    if (ess < (double)P / 2.0) {
+      const uint64_t lo = words[u0_idx], hi = words[u0_idx + 1];
+      const double u0 = (double)(((hi << 32) | lo) >> 11) * 0x1.0p-53;
+      pos += 2;
+      pf_resample<PPT>(s, k0, P, u0, S);
+      resampled = true;
     }
   }
+
+  if (B.trace_env == gi - B.env_index_offset && tid == 0)
+    printf("[trace env %lld set %d] nm=%d exact=%d have_ess=%d ess=%.17g resampled=%d pos=%llu\n",
+           (long long)(gi - B.env_index_offset), si, nm, (int)exact, (int)have_ess, ess, (int)resampled,
+           (unsigned long long)pos);
+
+  // ---- estimate (env.cpp:403-407)
+  const double3 est = pf_estimate<PPT>(s, k0, P, trk[K_EX * AT + si], trk[K_EY * AT + si], R);
+  store_set<PPT>(s, B, base, k0, P);
   if (tid == 0) {
     trk[K_EX * AT + si] = est.x;
     trk[K_EY * AT + si] = est.y;
@@ -536,8 +750,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     trk[K_AGE * AT + si] = fresh ? 0.0 : trk[K_AGE * AT + si] + 1.0;
     trk[K_EVER * AT + si] = (trk[K_EVER * AT + si] != 0.0 || fresh) ? 1.0 : 0.0;
     trk[K_POS * AT + si] = (double)pos;
-    *stat_upd += (double)n_upd;
-    *stat_res += resampled ? 1.0 : 0.0;
+    trk[K_ESSOK * AT + si] = 1.0;  // maybe_resample ran: ESS >= P/2 or weights uniform
+    stat[0] += (double)nm;
+    stat[1] += resampled ? 1.0 : 0.0;
   }
 }
 
@@ -545,19 +760,22 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 template <int PPT>
 __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int64_t gi,
                            int64_t gset, int si, double cx, double cy, double vmax) {
-  const int P = c.P, tid = threadIdx.x, NT = blockDim.x, AT = c.A * c.T;
+  const int P = c.P, tid = threadIdx.x, AT = c.A * c.T;
+  const int k0 = tid * PPT;
   double* trk = S.rec + c.o_track;
   uint64_t pos = (uint64_t)trk[K_POS * AT + si];
   const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)si);
-  uint32_t* words = reinterpret_cast<uint32_t*>(S.uni);
+  uint32_t* words = reinterpret_cast<uint32_t*>(S.cum);  // the resample area
+  __syncthreads();  // that area may still be read by the previous phase
   gen_words(words, key, (uint64_t)si, pos, 8ull * (uint64_t)P);
+  __syncthreads();
   const int off = (int)(pos & 3);
   const double inv = 1.0 / (double)P;
   const double radius = c.init_radius;
   SetRegs<PPT> s;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    const int k = tid + j * NT;
+    const int k = k0 + j;
     s.px[j] = s.py[j] = s.vx[j] = s.vy[j] = s.w[j] = 0.0;
     if (k < P) {
       const uint32_t* q = words + off + 8 * k;
@@ -581,19 +799,8 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
     }
   }
   pos += 8ull * (uint64_t)P;
-  const double3 est = pf_estimate<PPT>(s, P, R);
-  const size_t base = (size_t)gset * P;
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = tid + j * NT;
-    if (k < P) {
-      B.px[base + k] = s.px[j];
-      B.py[base + k] = s.py[j];
-      B.vx[base + k] = s.vx[j];
-      B.vy[base + k] = s.vy[j];
-      B.w[base + k] = s.w[j];
-    }
-  }
+  const double3 est = pf_estimate<PPT>(s, k0, P, cx, cy, R);
+  store_set<PPT>(s, B, (size_t)gset * P, k0, P);
   if (tid == 0) {
     trk[K_EX * AT + si] = est.x;
     trk[K_EY * AT + si] = est.y;
@@ -602,6 +809,7 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
     trk[K_EVER * AT + si] = 0.0;
     trk[K_POS * AT + si] = (double)pos;
     trk[K_MAXSPEED * AT + si] = vmax;
+    trk[K_ESSOK * AT + si] = 1.0;
   }
   __syncthreads();
 }
@@ -609,8 +817,8 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
 // ------------------------------------------------------------- spawn ---
 // Environment::spawn, serial part (env.cpp:155-212, 221-224). Thread 0 only.
 // Returns false when the rejection sampling fails (ConfigError in the reference).
-__device__ bool spawn_serial(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t gi) {
-  const int A = c.A, T = c.T, R = c.R, AA = A * A, AT = A * T;
+__device__ __noinline__ bool spawn_serial(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t gi) {
+  const int A = c.A, T = c.T, R = c.R, AA = A * A;
   double* rec = S.rec;
   double* ag = rec + c.o_agent;
   double* tg = rec + c.o_target;
@@ -665,7 +873,6 @@ __device__ bool spawn_serial(const DevConfig& c, const DevBatch& B, const Smem& 
   for (int f = 0; f < I_NFIELD; ++f)
     for (int i = 0; i < AA; ++i) info[f * AA + i] = 0.0;
   for (int t = 0; t < T; ++t) rec[c.o_miss + t] = 0.0;
-  (void)AT;
   rec[R_STEP] = 0.0;
   rec[R_EP_RETURN] = 0.0;
   rec[R_ENV_POS] = (double)rng.pos;
@@ -677,7 +884,7 @@ __device__ bool spawn_serial(const DevConfig& c, const DevBatch& B, const Smem& 
 // Full spawn: serial part + every set's re-init. All threads. Returns false on
 // spawn failure (CTA-uniform).
 template <int PPT>
-__device__ bool spawn_env(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int64_t e,
+__device__ __noinline__ bool spawn_env(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int64_t e,
                           int64_t gi) {
   if (threadIdx.x == 0) S.bc[8] = spawn_serial(c, B, S, gi) ? 1.0 : 0.0;
   __syncthreads();
@@ -695,7 +902,7 @@ __device__ bool spawn_env(const DevConfig& c, const DevBatch& B, const Smem& S, 
 // --------------------------------------------------------- outputs ---
 // build_observation (env.cpp:412-453) / build_global_state (env.cpp:455-471) for
 // env e into the batch layout (vecenv.cpp:47-56), plus masks (vecenv.cpp:58-67).
-__device__ void write_tokens(const DevConfig& c, const DevBatch& B, const double* rec, int64_t e, double* obs,
+__device__ __noinline__ void write_tokens(const DevConfig& c, const DevBatch& B, const double* rec, int64_t e, double* obs,
                              bool with_global, bool with_masks) {
   const int A = c.A, T = c.T, R = c.R, Am = B.A_max, Rm = B.R_max, AA = A * A, AT = A * T;
   const double* ag = rec + c.o_agent;
@@ -788,7 +995,7 @@ __device__ void write_tokens(const DevConfig& c, const DevBatch& B, const double
 
 // compute_reward_and_info (env.cpp:473-505) + VecEnv bookkeeping
 // (vecenv.cpp:95-104) + device statistics. Thread 0 only. Returns done.
-__device__ bool env_epilogue(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t e) {
+__device__ __noinline__ bool env_epilogue(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t e) {
   const int A = c.A, T = c.T, AT = A * T, Tm = B.T_max;
   double* rec = S.rec;
   const double* ag = rec + c.o_agent;
@@ -865,17 +1072,17 @@ __device__ bool env_epilogue(const DevConfig& c, const DevBatch& B, const Smem& 
   return done;
 }
 
-__device__ __forceinline__ void load_rec(double* dst, const double* src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
-}
-__device__ __forceinline__ void store_rec(double* dst, const double* src, int n) {
+__device__ __forceinline__ void copy_rec(double* dst, const double* src, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
 // ================================================================ kernels ===
 // The fused step: one CTA per env.
+#ifndef UT_STEP_MIN_BLOCKS
+#define UT_STEP_MIN_BLOCKS 2
+#endif
 template <int PPT>
-__global__ void step_kernel(DevBatch B, int mode, int32_t* status) {
+__global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t e = blockIdx.x;
   const DevConfig& c = cfg_of(B, e);
@@ -883,25 +1090,43 @@ __global__ void step_kernel(DevBatch B, int mode, int32_t* status) {
   BlockReducer R{S.red, 0};
   const int64_t gi = B.env_index_offset + e;
   double* grec = B.rec + rec_off(B, e);
-  load_rec(S.rec, grec, c.rec_words);
+  const long long tc0 = clock64();
+  load_tables(S);
+  copy_rec(S.rec, grec, c.rec_words);
   __syncthreads();
   if (threadIdx.x == 0) env_prologue(c, B, S, e, gi, mode);
+  // first set's words, generated while thread 0 runs the prologue
+  {
+    const int AT = c.A * c.T;
+    const uint64_t pos0 = (uint64_t)S.rec[c.o_track + K_POS * AT];
+    gen_words(S.words[0], derive_key(B.seed, kTagPf, (uint64_t)gi, 0), 0, pos0,
+              (c.noise_on ? 4ull * (uint64_t)c.P : 0ull) + 2ull);
+  }
   __syncthreads();
+
+  const long long tc1 = clock64();
 
   const int64_t so = set_off(B, e);
-  double stat_upd = 0.0, stat_res = 0.0;
+  double stat[3] = {0.0, 0.0, 0.0};
+  int wb = 0;
   for (int a = 0; a < c.A; ++a)
-    for (int t = 0; t < c.T; ++t) step_set<PPT>(c, B, S, R, gi, so + a * c.T + t, a, t, &stat_upd, &stat_res);
+    for (int t = 0; t < c.T; ++t) {
+      step_set<PPT>(c, B, S, R, gi, so + a * c.T + t, a, t, wb, stat);
+      wb ^= 1;
+    }
   __syncthreads();
+  const long long tc2 = clock64();
 
   if (threadIdx.x == 0) {
-    S.rec[c.o_stats + 7] += stat_upd;
-    S.rec[c.o_stats + 8] += stat_res;
+    S.rec[c.o_stats + 7] += stat[0];
+    S.rec[c.o_stats + 8] += stat[1];
+    S.rec[c.o_stats + 9] += stat[2];
     S.bc[9] = env_epilogue(c, B, S, e) ? 1.0 : 0.0;
   }
   __syncthreads();
   const bool done = S.bc[9] != 0.0;
   write_tokens(c, B, S.rec, e, B.obs, true, !done);
+  long long tc3 = clock64(), tc4 = tc3;
   if (done) {
     write_tokens(c, B, S.rec, e, B.final_obs, false, false);
     __syncthreads();
@@ -910,10 +1135,18 @@ __global__ void step_kernel(DevBatch B, int mode, int32_t* status) {
     }
     __syncthreads();
     write_tokens(c, B, S.rec, e, B.obs, true, true);
+    tc4 = clock64();
   }
   if (threadIdx.x == 0) B.step[e] = (int32_t)S.rec[R_STEP];
   __syncthreads();
-  store_rec(grec, S.rec, c.rec_words);
+  copy_rec(grec, S.rec, c.rec_words);
+  if (B.phase_cycles && threadIdx.x == 0) {
+    unsigned long long* pc = B.phase_cycles + e * kPhaseCount;
+    pc[PH_PROLOGUE] += (unsigned long long)(tc1 - tc0);
+    pc[PH_FILTER] += (unsigned long long)(tc2 - tc1);
+    pc[PH_OUTPUT] += (unsigned long long)(tc3 - tc2);
+    pc[PH_RESET] += (unsigned long long)(tc4 - tc3);
+  }
 }
 
 // Environment ctor / reset (env.cpp:110-151, 153-233) for every env. When
@@ -939,7 +1172,7 @@ __global__ void reset_kernel(DevBatch B, int ctor, int32_t* status) {
     for (int a = threadIdx.x; a < c.A; a += blockDim.x) S.rec[c.o_agent + V_RUDDER * c.A + a] = 2.0;
     for (int t = threadIdx.x; t < c.T; t += blockDim.x) S.rec[c.o_target + V_RUDDER * c.T + t] = 2.0;
   } else {
-    load_rec(S.rec, grec, c.rec_words);
+    copy_rec(S.rec, grec, c.rec_words);
   }
   __syncthreads();
   if (!spawn_env<PPT>(c, B, S, R, e, gi)) {
@@ -953,7 +1186,7 @@ __global__ void reset_kernel(DevBatch B, int ctor, int32_t* status) {
     B.step[e] = (int32_t)S.rec[R_STEP];
   }
   __syncthreads();
-  store_rec(grec, S.rec, c.rec_words);
+  copy_rec(grec, S.rec, c.rec_words);
 }
 
 // VecEnv::refresh_outputs (vecenv.cpp:145-150).
@@ -962,7 +1195,7 @@ __global__ void tokens_kernel(DevBatch B) {
   const int64_t e = blockIdx.x;
   const DevConfig& c = cfg_of(B, e);
   double* rec = reinterpret_cast<double*>(smem_raw);
-  load_rec(rec, B.rec + rec_off(B, e), c.rec_words);
+  copy_rec(rec, B.rec + rec_off(B, e), c.rec_words);
   __syncthreads();
   write_tokens(c, B, rec, e, B.obs, true, true);
   if (threadIdx.x == 0) B.step[e] = (int32_t)rec[R_STEP];
@@ -986,7 +1219,7 @@ __global__ void validate_kernel(DevBatch B) {
 
 // Sum of the per-env statistics (deterministic single-CTA tree), optional reset.
 __global__ void stats_kernel(DevBatch B, double* out, int reset) {
-  __shared__ double red[2 * 32 * 2];
+  __shared__ double red[kRedDoubles];
   BlockReducer R{red, 0};
   for (int k = 0; k < kStatCount; ++k) {
     double acc = 0.0;

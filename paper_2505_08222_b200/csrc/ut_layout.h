@@ -32,9 +32,12 @@ enum : int { V_X = 0, V_Y, V_Z, V_HEAD, V_SPEED, V_RUDDER, V_COUNTDOWN, V_CMD };
 // AgentInfo fields (env.hpp:19-25)
 enum : int { I_X = 0, I_Y, I_Z, I_HEAD, I_AGE, I_VALID, I_NFIELD };
 // track fields: TrackEstimate + ever_measured + PF RngStream::State + max_speed
-enum : int { K_EX = 0, K_EY, K_SPREAD, K_AGE, K_EVER, K_POS, K_HAVE_SPARE, K_SPARE, K_MAXSPEED, K_NFIELD };
+enum : int { K_EX = 0, K_EY, K_SPREAD, K_AGE, K_EVER, K_POS, K_HAVE_SPARE, K_SPARE, K_MAXSPEED,
+             K_ESSOK,  // not serialized: 1 when maybe_resample already vetted these weights
+             K_NFIELD };
+constexpr int K_NBLOB = 9;  // track fields carried by the state blob (env.cpp:578-583)
 
-constexpr int kStatCount = 9;  // ut_env.h UT_N_STATS
+constexpr int kStatCount = 10;  // ut_env.h UT_N_STATS
 
 // Resolved configuration for one fleet shape (EnvConfig after finalize()).
 struct DevConfig {
@@ -90,6 +93,18 @@ struct DevBatch {
   const int32_t* actions;
   int32_t* error_env;  // validation: lowest failing env (INT32_MAX if none)
   int32_t* error_info; // [3] agent, action, rudder of that env
+  // verification knobs (ut_debug.h): always take the exact sequential update
+  // path; printf a per-set trace for one env (-1 = off)
+  int32_t force_exact;
+  int64_t trace_env;
+  // Phase timing (PhaseTimer, env.cpp:18-36): SM cycles per env accumulated in
+  // [n_envs][kPhaseCount] when non-null.
+  unsigned long long* phase_cycles;
 };
+
+// Device phases (the reference's seven StepPhase values, env.hpp:71-80, map onto
+// these: targets+agents+measure+comm decisions -> PROLOGUE, filter+comm updates
+// -> FILTER, observe+reward -> OUTPUT, and auto-reset -> RESET).
+enum : int { PH_PROLOGUE = 0, PH_FILTER, PH_OUTPUT, PH_RESET, kPhaseCount };
 
 }  // namespace ut

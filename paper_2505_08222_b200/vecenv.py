@@ -333,6 +333,18 @@ class VecEnv:
         _check(self._lib.ut_vecenv_stats(self._h, out, int(reset)))
         return np.array(out[:])
 
+    PHASES = ("prologue", "filter", "output", "reset")
+
+    def enable_phase_timing(self, on: bool = True):
+        """VecEnv::enable_phase_timing (vecenv.hpp:64) on the device."""
+        _check(self._lib.ut_vecenv_enable_phase_timing(self._h, int(on)))
+
+    def phase_cycles(self, reset: bool = False) -> dict:
+        """SM cycles per device phase summed over envs (VecEnv::phase_ns analogue)."""
+        out = (C.c_uint64 * len(self.PHASES))()
+        _check(self._lib.ut_vecenv_phase_cycles(self._h, out, int(reset)))
+        return dict(zip(self.PHASES, out[:]))
+
     def launch_count(self) -> int:
         return int(self._lib.ut_vecenv_launch_count(self._h))
 

@@ -239,7 +239,8 @@ def test_device_stats_match_oracle(cuda_device):
     ora.step_policy(25)
     gpu.step_policy("random", 25)
     a, b = gpu.stats(), ora.stats()
-    assert np.allclose(a, b, rtol=1e-12, atol=1e-12), (a, b)
+    # all but the last slot (device-only: sets that took the exact update path)
+    assert np.allclose(a[:-1], b[:-1], rtol=1e-12, atol=1e-12), (a, b)
 
 
 def test_cr_math_exhaustive_on_device(cuda_device):
