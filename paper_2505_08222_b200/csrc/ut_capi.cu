@@ -66,7 +66,7 @@ bool default_bucket(double speed, double dt, double* a_out, double* b_out) {
   return true;
 }
 
-DevConfig to_dev(const ut_env_config& c) {
+DevConfig to_dev(const ut_env_config& c, int sA, int sT) {
   DevConfig d{};
   d.A = c.n_agents;
   d.T = c.n_targets;
@@ -102,25 +102,18 @@ DevConfig to_dev(const ut_env_config& c) {
   d.head_b = c.heading_b;
   d.head_noise = c.heading_noise_std;
   d.max_turn = c.max_turn_per_step;
-  layout_config(d);
+  layout_config(d, sA, sT);
   return d;
 }
 
 constexpr int kPPT = 4;
-constexpr int kMaxParticles = 4096;
+constexpr int kMaxParticles = 1024;  // 256 threads x 4 particles per CTA
 
 int threads_for(int P) {
   int nt = (P + kPPT - 1) / kPPT;
   nt = (nt + 31) / 32 * 32;
   return std::max(32, nt);
 }
-
-struct DeviceBuf {
-  void* p = nullptr;
-  ~DeviceBuf() {
-    if (p) cudaFree(p);
-  }
-};
 
 }  // namespace
 
@@ -134,15 +127,16 @@ struct ut_vecenv {
   std::vector<ut_env_config> cfgs;
   std::vector<DevConfig> dcfgs;
   std::vector<int32_t> cfg_of_env;  // empty: homogeneous
-  std::vector<int64_t> rec_off, set_off;
-  int64_t total_sets = 0, total_rec = 0;
-  int A_max = 0, T_max = 0, R_max = 0, P = 0, rec_words_max = 0;
-  int nt = 0;
+  std::vector<int64_t> set_off;
+  int64_t total_sets = 0;
+  int A_max = 0, T_max = 0, R_max = 0, P = 0, rec_words = 0;
+  int nt = 0, grid = 0;
   size_t smem = 0;
   DevBatch B{};
   std::vector<void*> allocs;
   int32_t* d_status = nullptr;  // [0] status, [1] error_env
   int32_t* h_status = nullptr;  // pinned
+  unsigned long long* phase_buf = nullptr;
   int64_t launches = 0;
 
   ~ut_vecenv() {
@@ -163,9 +157,23 @@ struct ut_vecenv {
     return UT_OK;
   }
 
-  DevConfig& cfg(int64_t e) { return dcfgs[cfg_of_env.empty() ? 0 : cfg_of_env[(size_t)e]]; }
-  int64_t rec_at(int64_t e) const { return rec_off[(size_t)e]; }
+  const DevConfig& cfg(int64_t e) const { return dcfgs[cfg_of_env.empty() ? 0 : cfg_of_env[(size_t)e]]; }
   int64_t set_at(int64_t e) const { return set_off[(size_t)e]; }
+
+  // One env's record column <-> host vector (rec[w * n_envs + e]).
+  int get_rec(int64_t e, std::vector<double>& out) {
+    out.resize((size_t)rec_words);
+    UT_CUDA(cudaStreamSynchronize(stream));
+    UT_CUDA(cudaMemcpy2D(out.data(), sizeof(double), B.rec + e, sizeof(double) * n_envs, sizeof(double), rec_words,
+                         cudaMemcpyDeviceToHost));
+    return UT_OK;
+  }
+  int put_rec(int64_t e, const std::vector<double>& in) {
+    UT_CUDA(cudaStreamSynchronize(stream));
+    UT_CUDA(cudaMemcpy2D(B.rec + e, sizeof(double) * n_envs, in.data(), sizeof(double), sizeof(double), rec_words,
+                         cudaMemcpyHostToDevice));
+    return UT_OK;
+  }
 
   int check_status(const char* what) {
     UT_CUDA(cudaMemcpyAsync(h_status, d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
@@ -185,14 +193,27 @@ struct ut_vecenv {
     return UT_OK;
   }
 
+  DevBatch* d_self = nullptr;  // device copy of B for the kernels' cold paths
+  bool full = false;           // P == nt * kPPT: TMA-prefetched register-tile path
+
+  // Publishes B to its device copy; call after any change to B.
+  int sync_batch() {
+    B.self = d_self;
+    UT_CUDA(cudaMemcpyAsync(d_self, &B, sizeof(DevBatch), cudaMemcpyHostToDevice, stream));
+    return UT_OK;
+  }
+
   int launch_step(int mode) {
-    step_kernel<kPPT><<<(unsigned)n_envs, nt, smem, stream>>>(B, mode, d_status);
+    if (full)
+      step_kernel<kPPT, true><<<(unsigned)grid, nt, smem, stream>>>(B, mode, d_status);
+    else
+      step_kernel<kPPT, false><<<(unsigned)grid, nt, smem, stream>>>(B, mode, d_status);
     ++launches;
     UT_CUDA(cudaGetLastError());
     return UT_OK;
   }
   int launch_reset(int ctor) {
-    reset_kernel<kPPT><<<(unsigned)n_envs, nt, smem, stream>>>(B, ctor, d_status);
+    reset_kernel<kPPT><<<(unsigned)grid, nt, smem, stream>>>(B, ctor, d_status);
     ++launches;
     UT_CUDA(cudaGetLastError());
     return UT_OK;
@@ -204,7 +225,6 @@ namespace {
 int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg_of_env, int64_t n_envs,
           uint64_t seed, int64_t offset, int device) {
   if (n_envs < 1) return fail(UT_ERR_CONFIG, "vecenv: n_envs must be >= 1");
-  if (n_envs > INT_MAX) return fail(UT_ERR_CONFIG, "vecenv: n_envs must fit a CUDA grid");
   v->device = device;
   v->n_envs = n_envs;
   v->offset = offset;
@@ -215,30 +235,27 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
     if (rc) return rc;
     if (c.pf.n_particles > kMaxParticles)
       return fail(UT_ERR_CONFIG, "env.pf.n_particles must be <= %d on this device build", kMaxParticles);
+    if (c.n_agents + c.n_targets > kMaxEntities)
+      return fail(UT_ERR_CONFIG, "env.n_agents + env.n_targets must be <= %d on this device build", kMaxEntities);
     if (i > 0 && c.pf.n_particles != cfgs[0].pf.n_particles)
       return fail(UT_ERR_CONFIG, "mixed fleets must share env.pf.n_particles");
     v->cfgs.push_back(c);
-    v->dcfgs.push_back(to_dev(c));
+    v->A_max = std::max(v->A_max, c.n_agents);
+    v->T_max = std::max(v->T_max, c.n_targets);
+    v->R_max = std::max(v->R_max, c.n_agents + c.n_targets);
   }
+  for (const ut_env_config& c : v->cfgs) v->dcfgs.push_back(to_dev(c, v->A_max, v->T_max));
+  v->rec_words = v->dcfgs[0].rec_words;
   if (cfg_of_env) {
     v->cfg_of_env.assign(cfg_of_env, cfg_of_env + n_envs);
     for (int32_t k : v->cfg_of_env)
       if (k < 0 || k >= n_cfg) return fail(UT_ERR_CONFIG, "cfg_of_env index %d out of range", k);
   }
-  for (const DevConfig& d : v->dcfgs) {
-    v->A_max = std::max(v->A_max, d.A);
-    v->T_max = std::max(v->T_max, d.T);
-    v->R_max = std::max(v->R_max, d.R);
-    v->rec_words_max = std::max(v->rec_words_max, d.rec_words);
-  }
   v->P = v->dcfgs[0].P;
-  v->rec_off.resize((size_t)n_envs);
   v->set_off.resize((size_t)n_envs);
   for (int64_t e = 0; e < n_envs; ++e) {
     const DevConfig& d = v->cfg(e);
-    v->rec_off[(size_t)e] = v->total_rec;
     v->set_off[(size_t)e] = v->total_sets;
-    v->total_rec += d.rec_words;
     v->total_sets += (int64_t)d.A * d.T;
   }
 
@@ -266,19 +283,18 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   B.cfgs = dc;
   if (!v->cfg_of_env.empty()) {
     int32_t* ce;
-    int64_t *ro, *so;
+    int64_t* so;
     if ((rc = v->alloc(&ce, (size_t)n_envs))) return rc;
-    if ((rc = v->alloc(&ro, (size_t)n_envs))) return rc;
     if ((rc = v->alloc(&so, (size_t)n_envs))) return rc;
     UT_CUDA(cudaMemcpy(ce, v->cfg_of_env.data(), sizeof(int32_t) * n_envs, cudaMemcpyHostToDevice));
-    UT_CUDA(cudaMemcpy(ro, v->rec_off.data(), sizeof(int64_t) * n_envs, cudaMemcpyHostToDevice));
     UT_CUDA(cudaMemcpy(so, v->set_off.data(), sizeof(int64_t) * n_envs, cudaMemcpyHostToDevice));
     B.cfg_of_env = ce;
-    B.rec_offset = ro;
     B.set_offset = so;
   }
   const size_t np = (size_t)(v->total_sets * P);
-  if ((rc = v->alloc(&B.rec, (size_t)v->total_rec))) return rc;
+  if ((rc = v->alloc(&B.rec, (size_t)v->rec_words * (size_t)n_envs))) return rc;
+  if ((rc = v->alloc(&B.sched_r2, (size_t)(n_envs * Am * Tm)))) return rc;
+  if ((rc = v->alloc(&B.sched_flags, (size_t)(n_envs * (Am * Tm + Am * Am))))) return rc;
   if ((rc = v->alloc(&B.px, np))) return rc;
   if ((rc = v->alloc(&B.py, np))) return rc;
   if ((rc = v->alloc(&B.vx, np))) return rc;
@@ -311,17 +327,29 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   UT_CUDA(cudaMemsetAsync(B.lost, 0, n_envs * Tm, v->stream));
   UT_CUDA(cudaMemsetAsync(B.collision, 0, n_envs, v->stream));
   UT_CUDA(cudaMemsetAsync(acts, 0, sizeof(int32_t) * n_envs * Am, v->stream));
+  UT_CUDA(cudaMemsetAsync(B.sched_flags, 0, n_envs * (Am * Tm + Am * Am), v->stream));
 
   v->nt = threads_for(v->P);
-  v->smem = smem_bytes(v->rec_words_max, v->A_max, v->T_max, v->P);
-  int max_optin = 0;
+  v->smem = smem_bytes(v->A_max, v->T_max, v->P, v->nt);
+  int max_optin = 0, sms = 0;
   UT_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   if ((int)v->smem > max_optin)
-    return fail(UT_ERR_CONFIG, "configuration needs %zu B of shared memory per env (max %d)", v->smem, max_optin);
-  UT_CUDA(cudaFuncSetAttribute(step_kernel<kPPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
+    return fail(UT_ERR_CONFIG, "configuration needs %zu B of shared memory per CTA (max %d)", v->smem, max_optin);
+  v->full = (v->P == v->nt * kPPT) && (v->P % 4 == 0);
+  UT_CUDA(cudaFuncSetAttribute(step_kernel<kPPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
+  UT_CUDA(cudaFuncSetAttribute(step_kernel<kPPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
   UT_CUDA(cudaFuncSetAttribute(reset_kernel<kPPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
-  UT_CUDA(cudaFuncSetAttribute(tokens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(sizeof(double) * v->rec_words_max)));
+  // persistent grid: every resident CTA slot, each owning a contiguous env range
+  int per_sm = 0;
+  if (v->full)
+    UT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<kPPT, true>, v->nt, v->smem));
+  else
+    UT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<kPPT, false>, v->nt, v->smem));
+  if (per_sm < 1) return fail(UT_ERR_RUNTIME, "step kernel cannot be resident with %zu B shared memory", v->smem);
+  v->grid = (int)std::min<int64_t>(n_envs, (int64_t)per_sm * sms);
+  if ((rc = v->alloc(&v->d_self, 1))) return rc;
+  if ((rc = v->sync_batch())) return rc;
 
   // Environment ctors: pf::init draws, then spawn (env.cpp:110-151)
   if ((rc = v->reset_status())) return rc;
@@ -329,11 +357,14 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   return v->check_status("vecenv ctor");
 }
 
-int host_rudders(ut_vecenv* v, int64_t e, std::vector<double>& out) {
-  const DevConfig& d = v->cfg(e);
-  out.resize((size_t)d.A);
-  UT_CUDA(cudaMemcpy(out.data(), v->B.rec + v->rec_at(e) + d.o_agent + V_RUDDER * d.A, sizeof(double) * d.A,
-                     cudaMemcpyDeviceToHost));
+int finish_create(ut_vecenv* v, int rc, ut_vecenv** out) {
+  if (rc) {
+    const std::string msg = g_err;
+    delete v;
+    g_err = msg;
+    return rc;
+  }
+  *out = v;
   return UT_OK;
 }
 
@@ -415,15 +446,7 @@ int ut_vecenv_create(const ut_env_config* cfg, int64_t n_envs, uint64_t master_s
                      int device, ut_vecenv** out) {
   *out = nullptr;
   auto* v = new ut_vecenv();
-  const int rc = build(v, cfg, 1, nullptr, n_envs, master_seed, env_index_offset, device);
-  if (rc) {
-    const std::string msg = g_err;
-    delete v;
-    g_err = msg;
-    return rc;
-  }
-  *out = v;
-  return UT_OK;
+  return finish_create(v, build(v, cfg, 1, nullptr, n_envs, master_seed, env_index_offset, device), out);
 }
 
 int ut_vecenv_create_mixed(const ut_env_config* cfgs, int32_t n_cfgs, const int32_t* cfg_of_env, int64_t n_envs,
@@ -431,15 +454,7 @@ int ut_vecenv_create_mixed(const ut_env_config* cfgs, int32_t n_cfgs, const int3
   *out = nullptr;
   if (n_cfgs < 1 || !cfg_of_env) return fail(UT_ERR_CONFIG, "mixed vecenv needs >= 1 config and a cfg_of_env map");
   auto* v = new ut_vecenv();
-  const int rc = build(v, cfgs, n_cfgs, cfg_of_env, n_envs, master_seed, env_index_offset, device);
-  if (rc) {
-    const std::string msg = g_err;
-    delete v;
-    g_err = msg;
-    return rc;
-  }
-  *out = v;
-  return UT_OK;
+  return finish_create(v, build(v, cfgs, n_cfgs, cfg_of_env, n_envs, master_seed, env_index_offset, device), out);
 }
 
 void ut_vecenv_destroy(ut_vecenv* v) { delete v; }
@@ -467,10 +482,11 @@ int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device) 
     const int64_t e = v->h_status[1];
     std::vector<int32_t> acts((size_t)v->A_max);
     UT_CUDA(cudaMemcpy(acts.data(), v->B.actions + e * v->A_max, sizeof(int32_t) * v->A_max, cudaMemcpyDeviceToHost));
-    std::vector<double> rud;
-    if ((rc = host_rudders(v, e, rud))) return rc;
-    for (int a = 0; a < v->cfg(e).A; ++a) {
-      const int act = acts[(size_t)a], r = (int)rud[(size_t)a];
+    std::vector<double> rec;
+    if ((rc = v->get_rec(e, rec))) return rc;
+    const DevConfig& d = v->cfg(e);
+    for (int a = 0; a < d.A; ++a) {
+      const int act = acts[(size_t)a], r = (int)rec[(size_t)(d.o_agent + V_RUDDER * d.sA + a)];
       if (act < 0 || act >= UT_NUM_ACTIONS || std::abs(act - r) > 1)
         return fail(UT_ERR_CONTRACT, "env %lld: step: invalid action %d for agent %d at rudder index %d", (long long)e,
                     act, a, r);
@@ -492,7 +508,9 @@ int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps) {
 }
 
 int ut_vecenv_refresh_outputs(ut_vecenv* v) {
-  tokens_kernel<<<(unsigned)v->n_envs, 64, sizeof(double) * v->rec_words_max, v->stream>>>(v->B);
+  int sms = 0;
+  UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, v->device));
+  tokens_kernel<<<(unsigned)(sms * 8), 256, 0, v->stream>>>(v->B);
   ++v->launches;
   UT_CUDA(cudaGetLastError());
   UT_CUDA(cudaStreamSynchronize(v->stream));
@@ -577,27 +595,25 @@ int64_t ut_vecenv_launch_count(const ut_vecenv* v) { return v->launches; }
 
 int ut_vecenv_enable_phase_timing(ut_vecenv* v, int on) {
   UT_CUDA(cudaStreamSynchronize(v->stream));
-  if (on && !v->B.phase_cycles) {
-    unsigned long long* p;
+  if (on && !v->phase_buf) {
     int rc;
-    if ((rc = v->alloc(&p, (size_t)(v->n_envs * kPhaseCount)))) return rc;
-    UT_CUDA(cudaMemset(p, 0, sizeof(unsigned long long) * v->n_envs * kPhaseCount));
-    v->B.phase_cycles = p;
-  } else if (!on) {
-    v->B.phase_cycles = nullptr;  // buffer stays owned by the handle
+    if ((rc = v->alloc(&v->phase_buf, (size_t)v->grid * kPhaseCount))) return rc;
+    UT_CUDA(cudaMemset(v->phase_buf, 0, sizeof(unsigned long long) * v->grid * kPhaseCount));
   }
-  return UT_OK;
+  v->B.phase_cycles = on ? v->phase_buf : nullptr;
+  return v->sync_batch();
 }
 
+// Per-CTA phase cycles summed over the grid (each CTA steps a contiguous env
+// range, so this is the device analogue of the per-env phase sums).
 int ut_vecenv_phase_cycles(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset) {
   for (int k = 0; k < UT_N_PHASES; ++k) out[k] = 0;
-  if (!v->B.phase_cycles) return UT_OK;
+  if (!v->phase_buf) return UT_OK;
   UT_CUDA(cudaStreamSynchronize(v->stream));
-  std::vector<unsigned long long> h((size_t)(v->n_envs * kPhaseCount));
-  UT_CUDA(cudaMemcpy(h.data(), v->B.phase_cycles, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
-  for (int64_t e = 0; e < v->n_envs; ++e)
-    for (int k = 0; k < kPhaseCount; ++k) out[k] += h[(size_t)(e * kPhaseCount + k)];
-  if (reset) UT_CUDA(cudaMemset(v->B.phase_cycles, 0, sizeof(unsigned long long) * h.size()));
+  std::vector<unsigned long long> h((size_t)v->grid * kPhaseCount);
+  UT_CUDA(cudaMemcpy(h.data(), v->phase_buf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < h.size(); ++i) out[i % kPhaseCount] += h[i];
+  if (reset) UT_CUDA(cudaMemset(v->phase_buf, 0, sizeof(unsigned long long) * h.size()));
   return UT_OK;
 }
 
@@ -605,15 +621,15 @@ int ut_vecenv_phase_cycles(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset) {
 int ut_env_serialize(ut_vecenv* v, int64_t e, double* blob, size_t cap, size_t* len) {
   if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "serialize: env %lld out of range", (long long)e);
   const DevConfig& d = v->cfg(e);
-  const int A = d.A, T = d.T, P = d.P, AA = A * A, AT = A * T;
+  const int A = d.A, T = d.T, P = d.P, sA = d.sA, sT = d.sT, AA = sA * sA, AT = sA * sT;
   const size_t need = (size_t)(5 + 6 * A + 9 * T + A * (6 * A + T * (9 + 5 * P)));
   *len = need;
   if (!blob) return UT_OK;
   if (cap < need) return fail(UT_ERR_DATA, "serialize: buffer of %zu doubles too small (need %zu)", cap, need);
-  UT_CUDA(cudaStreamSynchronize(v->stream));
-  std::vector<double> rec((size_t)d.rec_words);
-  UT_CUDA(cudaMemcpy(rec.data(), v->B.rec + v->rec_at(e), sizeof(double) * d.rec_words, cudaMemcpyDeviceToHost));
-  const size_t nset = (size_t)AT * P;
+  std::vector<double> rec;
+  int rc;
+  if ((rc = v->get_rec(e, rec))) return rc;
+  const size_t nset = (size_t)A * T * P;
   std::vector<double> f[5];
   double* src[5] = {v->B.px, v->B.py, v->B.vx, v->B.vy, v->B.w};
   for (int k = 0; k < 5; ++k) {
@@ -631,18 +647,18 @@ int ut_env_serialize(ut_vecenv* v, int64_t e, double* blob, size_t cap, size_t* 
   blob[i++] = rec[R_ENV_HAVE_SPARE];
   blob[i++] = rec[R_ENV_SPARE];
   for (int a = 0; a < A; ++a)
-    for (int fl = 0; fl < 6; ++fl) blob[i++] = ag[fl * A + a];
+    for (int fl = 0; fl < 6; ++fl) blob[i++] = ag[fl * sA + a];
   for (int t = 0; t < T; ++t)
-    for (int fl = 0; fl < 8; ++fl) blob[i++] = tg[fl * T + t];
+    for (int fl = 0; fl < 8; ++fl) blob[i++] = tg[fl * sT + t];
   for (int t = 0; t < T; ++t) blob[i++] = rec[(size_t)d.o_miss + t];
   for (int a = 0; a < A; ++a) {
     for (int j = 0; j < A; ++j)
-      for (int fl = 0; fl < I_NFIELD; ++fl) blob[i++] = info[fl * AA + a * A + j];
+      for (int fl = 0; fl < I_NFIELD; ++fl) blob[i++] = info[fl * AA + a * sA + j];
     for (int t = 0; t < T; ++t) {
-      const int si = a * T + t;
-      for (int fl = 0; fl < K_NBLOB; ++fl) blob[i++] = trk[fl * AT + si];
+      for (int fl = 0; fl < K_NBLOB; ++fl) blob[i++] = trk[fl * AT + a * sT + t];
+      const size_t ps = (size_t)(a * T + t);
       for (int k = 0; k < 5; ++k) {
-        std::memcpy(blob + i, f[k].data() + (size_t)si * P, sizeof(double) * P);
+        std::memcpy(blob + i, f[k].data() + ps * P, sizeof(double) * P);
         i += (size_t)P;
       }
     }
@@ -655,18 +671,18 @@ int ut_env_serialize(ut_vecenv* v, int64_t e, double* blob, size_t cap, size_t* 
 int ut_env_deserialize(ut_vecenv* v, int64_t e, const double* blob, size_t len) {
   if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "deserialize: env %lld out of range", (long long)e);
   const DevConfig& d = v->cfg(e);
-  const int A = d.A, T = d.T, P = d.P, AA = A * A, AT = A * T;
+  const int A = d.A, T = d.T, P = d.P, sA = d.sA, sT = d.sT, AA = sA * sA, AT = sA * sT;
   const size_t need = (size_t)(5 + 6 * A + 9 * T + A * (6 * A + T * (9 + 5 * P)));
   if (len < need) return fail(UT_ERR_DATA, "environment state blob truncated");
   if (len > need) return fail(UT_ERR_DATA, "environment state blob has trailing data");
-  UT_CUDA(cudaStreamSynchronize(v->stream));
-  std::vector<double> rec((size_t)d.rec_words);
-  UT_CUDA(cudaMemcpy(rec.data(), v->B.rec + v->rec_at(e), sizeof(double) * d.rec_words, cudaMemcpyDeviceToHost));
+  std::vector<double> rec;
+  int rc;
+  if ((rc = v->get_rec(e, rec))) return rc;
   double* ag = rec.data() + d.o_agent;
   double* tg = rec.data() + d.o_target;
   double* info = rec.data() + d.o_info;
   double* trk = rec.data() + d.o_track;
-  const size_t nset = (size_t)AT * P;
+  const size_t nset = (size_t)A * T * P;
   std::vector<double> f[5];
   for (auto& x : f) x.resize(nset);
   size_t i = 0;
@@ -680,39 +696,40 @@ int ut_env_deserialize(ut_vecenv* v, int64_t e, const double* blob, size_t len) 
   for (int a = 0; a < A; ++a)
     for (int fl = 0; fl < 6; ++fl) {
       const double x = blob[i++];
-      ag[fl * A + a] = fl == V_RUDDER ? as_int(x) : x;
+      ag[fl * sA + a] = fl == V_RUDDER ? as_int(x) : x;
     }
   for (int t = 0; t < T; ++t)
     for (int fl = 0; fl < 8; ++fl) {
       const double x = blob[i++];
-      tg[fl * T + t] = (fl == V_RUDDER || fl == V_COUNTDOWN) ? as_int(x) : x;
+      tg[fl * sT + t] = (fl == V_RUDDER || fl == V_COUNTDOWN) ? as_int(x) : x;
     }
   for (int t = 0; t < T; ++t) rec[(size_t)d.o_miss + t] = as_int(blob[i++]);
   for (int a = 0; a < A; ++a) {
     for (int j = 0; j < A; ++j)
       for (int fl = 0; fl < I_NFIELD; ++fl) {
         const double x = blob[i++];
-        double& dst = info[fl * AA + a * A + j];
+        double& dst = info[fl * AA + a * sA + j];
         dst = fl == I_AGE ? as_int(x) : fl == I_VALID ? (x != 0.0 ? 1.0 : 0.0) : x;
       }
     for (int t = 0; t < T; ++t) {
-      const int si = a * T + t;
+      const int ti = a * sT + t;
       for (int fl = 0; fl < K_NBLOB; ++fl) {
         const double x = blob[i++];
-        double& dst = trk[fl * AT + si];
+        double& dst = trk[fl * AT + ti];
         dst = fl == K_AGE ? as_int(x)
               : (fl == K_EVER || fl == K_HAVE_SPARE) ? (x != 0.0 ? 1.0 : 0.0)
               : fl == K_POS ? (double)(uint64_t)x
                             : x;
       }
-      trk[K_ESSOK * AT + si] = 0.0;  // injected weights have not been vetted
+      trk[K_ESSOK * AT + ti] = 0.0;  // injected weights have not been vetted
+      const size_t ps = (size_t)(a * T + t);
       for (int k = 0; k < 5; ++k) {
-        std::memcpy(f[k].data() + (size_t)si * P, blob + i, sizeof(double) * P);
+        std::memcpy(f[k].data() + ps * P, blob + i, sizeof(double) * P);
         i += (size_t)P;
       }
     }
   }
-  UT_CUDA(cudaMemcpy(v->B.rec + v->rec_at(e), rec.data(), sizeof(double) * d.rec_words, cudaMemcpyHostToDevice));
+  if ((rc = v->put_rec(e, rec))) return rc;
   double* dst[5] = {v->B.px, v->B.py, v->B.vx, v->B.vy, v->B.w};
   for (int k = 0; k < 5; ++k)
     UT_CUDA(cudaMemcpy(dst[k] + (size_t)v->set_at(e) * P, f[k].data(), sizeof(double) * nset, cudaMemcpyHostToDevice));
@@ -723,7 +740,7 @@ int ut_env_world_step(ut_vecenv* v, int64_t e, int32_t* step) {
   if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "world_step: env %lld out of range", (long long)e);
   double s = 0.0;
   UT_CUDA(cudaStreamSynchronize(v->stream));
-  UT_CUDA(cudaMemcpy(&s, v->B.rec + v->rec_at(e) + R_STEP, sizeof(double), cudaMemcpyDeviceToHost));
+  UT_CUDA(cudaMemcpy(&s, v->B.rec + (int64_t)R_STEP * v->n_envs + e, sizeof(double), cudaMemcpyDeviceToHost));
   *step = (int32_t)s;
   return UT_OK;
 }
@@ -777,6 +794,24 @@ __global__ void cr_grid_kernel(int kind, float* out) {
     out[i] = kind == 1 ? c : s;
   }
 }
+// The production (table-driven) path: fills both grids' results through
+// box_muller_fast, falling back exactly like the step kernel does.
+__global__ void cr_grid_fast_kernel(int kind, float* out) {
+  __shared__ double2 tl[128], ts[64];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tl[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) ts[i] = make_double2(kSinCosTab[2 * i], kSinCosTab[2 * i + 1]);
+  __syncthreads();
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (1u << 24)) return;
+  const float two_pi_f = 2.0f * 3.14159265358979323846f;
+  if (kind == 0) {
+    out[i] = cr_logf_fast((float)(i + 1u) * 0x1.0p-24f, tl);
+  } else {
+    float s, c;
+    cr_sincosf_fast(__fmul_rn(two_pi_f, (float)i * 0x1.0p-24f), &s, &c, ts);
+    out[i] = kind == 1 ? c : s;
+  }
+}
 __global__ void philox_kernel(uint64_t key, uint64_t stream, uint64_t block0, int n, uint4* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = philox(key, stream, block0 + (uint64_t)i);
@@ -792,7 +827,7 @@ extern "C" {
 int ut_debug_set_knobs(ut_vecenv* v, int force_exact, int64_t trace_env) {
   v->B.force_exact = force_exact;
   v->B.trace_env = trace_env;
-  return UT_OK;
+  return v->sync_batch();
 }
 int ut_debug_abi_sizes(int64_t out[4]) {
   out[0] = sizeof(ut_env_config);
@@ -806,7 +841,10 @@ int ut_debug_cr_grid(int kind, int device, float* host_out) {
   float* d = nullptr;
   const size_t n = (size_t)1 << 24;
   UT_CUDA(cudaMalloc(&d, n * sizeof(float)));
-  cr_grid_kernel<<<(unsigned)(n / 256), 256>>>(kind, d);
+  if (kind < 3)
+    cr_grid_kernel<<<(unsigned)(n / 256), 256>>>(kind, d);
+  else
+    cr_grid_fast_kernel<<<(unsigned)(n / 256), 256>>>(kind - 3, d);
   cudaError_t err = cudaMemcpy(host_out, d, n * sizeof(float), cudaMemcpyDeviceToHost);
   cudaFree(d);
   UT_CUDA(err);

@@ -1,20 +1,25 @@
 // ut_kernels.cuh -- the fused environment-step kernel and its helpers.
 //
-// One CTA steps one environment end to end (north_star "one fused kernel per
-// step"): the env record is staged in shared memory, one thread runs the serial
-// env-stream prologue (Appendix A order: targets, agents, pings, comm drops),
-// then the whole CTA runs every particle set of the env with the set held in
-// registers -- PPT consecutive particles per thread (128-bit coalesced loads and
-// stores, each set read once and written once per step) -- then the epilogue
-// (reward, done, tokens, masks) and, for finished envs, the auto-reset (spawn +
-// particle re-init) before the record is written back.
+// One persistent launch per step ("one fused kernel per step", north_star). Each
+// CTA owns a contiguous range of envs and walks it in chunks of blockDim.x envs:
 //
-// Per set the work is: predict (Philox words generated one set ahead into a
-// double-buffered smem area, correctly rounded fp32 Box-Muller), ONE merged pass
-// for all of this step's range updates (per-stage maxima kept so the reference's
-// sequential semantics hold; the exact sequential path runs whenever an
-// intermediate underflow could matter), ESS from the same reduction, systematic
-// resample (scan + search), estimate in one shifted reduction.
+//   1. PROLOGUE  one env per THREAD: actions, move_targets, move_agents,
+//      measure_ranges and the comm-drop decisions, in the reference's serial
+//      env-stream order, on that env's structure-of-arrays
+//      record (coalesced across the threads of the chunk). The ping schedule is
+//      handed to phase 2 through a small per-env scratch.
+//   2. FILTER    the whole CTA streams through every particle set of the chunk's
+//      envs (sets of consecutive envs are contiguous in HBM), each set held in
+//      registers -- PPT consecutive particles per thread, 128-bit loads/stores,
+//      read once and written once per step: predict (Philox words generated one
+//      set ahead, correctly rounded fp32 Box-Muller), ONE merged pass for all of
+//      the set's range updates (the reference's sequential semantics preserved,
+//      exact sequential path when an intermediate underflow could matter), ESS
+//      from the same reduction, systematic resample, estimate.
+//   3. OUTPUT    one env per thread: reward, done, info, stats; then tokens,
+//      global state and masks with one thread per token row.
+//   4. RESET     finished envs: spawn (one env per thread) + particle re-init
+//      (whole CTA per set) + fresh tokens.
 #pragma once
 #include "ut_device.cuh"
 
@@ -22,100 +27,111 @@ namespace ut {
 
 enum StepMode : int { MODE_EXTERNAL = -1, MODE_RANDOM = 0, MODE_SCRIPTED = 1 };
 enum DevStatus : int { ST_OK = 0, ST_SPAWN_INFEASIBLE = 2 };
-constexpr int kMaxMerged = 8;   // merged update handles up to 8 measurements per set
-constexpr int kMeasStride = 8;  // ox, oy, r2, sigma, 1/sigma (+pad)
+constexpr int kMaxMerged = 8;     // merged update handles up to 8 measurements per set
+constexpr int kMeasStride = 8;    // ox, oy, r2, sigma, 1/sigma (+pad)
+constexpr int kMaxEntities = 64;  // spawn scratch per thread
 constexpr double kMergeFloor = 0x1p-860;  // see the merged-update argument in step_set
+constexpr int kChunkFlagDone = 1, kChunkFlagSpawned = 2;
+
+// Strided view of one env's record: word w at p[w * n_envs].
+struct Rec {
+  double* p;
+  int64_t s;
+  __device__ __forceinline__ double& operator[](int w) const { return p[(int64_t)w * s]; }
+};
+__device__ __forceinline__ Rec rec_of(const DevBatch& B, int64_t e) { return Rec{B.rec + e, B.n_envs}; }
+
+#define AG(f, a) rec[c.o_agent + (f) * c.sA + (a)]
+#define TG(f, t) rec[c.o_target + (f) * c.sT + (t)]
+#define INFO(f, k) rec[c.o_info + (f) * c.sA * c.sA + (k)]
+#define TRK(f, ti) rec[c.o_track + (f) * c.sA * c.sT + (ti)]
+#define STAT(k) rec[c.o_stats + (k)]
 
 // ------------------------------------------------------------ smem carve ---
 struct Smem {
-  double2* tab_log;    // [128]
-  double2* tab_sc;     // [64]
-  double* rec;
-  double* meas;        // [A*T][kMeasStride]
-  double* red;         // kRedDoubles: BlockReducer buffers + scan warp sums
-  double* bc;          // 16 broadcast slots
-  double* qxy;         // [2 * R] spawn scratch
-  int* act;            // [A]
-  uint8_t* present;    // [A*T]
-  uint8_t* link;       // [A*A]
-  uint8_t* mcount;     // [A*T] measurements applied to each set this step
-  uint8_t* mlist;      // [A*T][A] their meas indices in application order
-  uint32_t* words[2];  // Philox words, double buffered: 4P + 2 (+ 8 slack)
-  double* cum;         // [P] resample scan
-  double* st;          // [4P] resample staging
+  double2* tab_log;  // [128]
+  double2* tab_sc;   // [64]
+  double* tab_exp;   // [32]
+  DevConfig* cfg;    // config of the env being filtered
+  double* red;       // kRedDoubles: BlockReducer buffers + scan warp sums
+  double* bc;        // 16 broadcast slots
+  uint4* xch;        // [32 warps][5] lane-0 Philox blocks (misaligned streams)
+  double* meas;      // [sA*sT][kMeasStride] pings of the env being filtered
+  uint16_t* mcount;  // [sA*sT] measurements applied to each set this step
+  uint16_t* mlist;   // [sA*sT][sA] their meas indices in application order
+  uint8_t* flags;    // [blockDim] per-env chunk flags
+  uint64_t* mbar;    // TMA completion barrier
+  double* pf;        // [5][P] TMA-prefetched next particle set
+  double* cum;       // [P] resample scan | re-init words
+  double* st;        // [4P] resample staging
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline size_t words_bytes(int P) {
-  // predict uses 4P words + 2 for the resample u0; one extra block covers a
-  // misaligned start. (Re-init's 8P words use the resample area instead.)
-  return align16((size_t)4 * (4 * (size_t)P + 2 + 8));
-}
 __host__ __device__ inline size_t resample_bytes(int P) {
-  const size_t a = sizeof(double) * 5 * (size_t)P;  // cum + 4 staged fields
+  const size_t a = sizeof(double) * 5 * (size_t)P;   // cum + 4 staged fields
   const size_t b = (size_t)4 * (8 * (size_t)P + 8);  // re-init words
   return align16(a > b ? a : b);
 }
 
-__host__ __device__ inline size_t smem_bytes(int rec_words, int A, int T, int P) {
-  const int R = A + T;
+__host__ __device__ inline size_t smem_bytes(int sA, int sT, int P, int nt) {
   size_t s = 0;
-  s += sizeof(double2) * (128 + 64);
-  s += align16(sizeof(double) * rec_words);
-  s += align16(sizeof(double) * kMeasStride * A * T);
+  s += sizeof(double2) * (128 + 64) + sizeof(double) * 32;
+  s += align16(sizeof(DevConfig));
   s += align16(sizeof(double) * kRedDoubles);
   s += align16(sizeof(double) * 16);
-  s += align16(sizeof(double) * 2 * R);
-  s += align16(sizeof(int) * A);
-  s += align16(A * T) + align16(A * A) + align16(A * T) + align16(A * T * A);
-  s += 2 * words_bytes(P);
+  s += sizeof(uint4) * 32 * 5;
+  s += align16(sizeof(double) * kMeasStride * sA * sT);
+  s += align16(sizeof(uint16_t) * sA * sT);
+  s += align16(sizeof(uint16_t) * sA * sT * sA);
+  s += align16(nt);
+  s += 16;
+  s += align16(sizeof(double) * 5 * (size_t)P);
   s += resample_bytes(P);
   return s;
 }
 
-__device__ inline Smem carve(unsigned char* base, int rec_words, int A, int T, int P) {
+__device__ inline Smem carve(unsigned char* base, int sA, int sT, int P) {
   Smem S;
-  const int R = A + T;
   size_t o = 0;
   S.tab_log = (double2*)(base + o);
   o += sizeof(double2) * 128;
   S.tab_sc = (double2*)(base + o);
   o += sizeof(double2) * 64;
-  S.rec = (double*)(base + o);
-  o += align16(sizeof(double) * rec_words);
-  S.meas = (double*)(base + o);
-  o += align16(sizeof(double) * kMeasStride * A * T);
+  S.tab_exp = (double*)(base + o);
+  o += sizeof(double) * 32;
+  S.cfg = (DevConfig*)(base + o);
+  o += align16(sizeof(DevConfig));
   S.red = (double*)(base + o);
   o += align16(sizeof(double) * kRedDoubles);
   S.bc = (double*)(base + o);
   o += align16(sizeof(double) * 16);
-  S.qxy = (double*)(base + o);
-  o += align16(sizeof(double) * 2 * R);
-  S.act = (int*)(base + o);
-  o += align16(sizeof(int) * A);
-  S.present = base + o;
-  o += align16(A * T);
-  S.link = base + o;
-  o += align16(A * A);
-  S.mcount = base + o;
-  o += align16(A * T);
-  S.mlist = base + o;
-  o += align16(A * T * A);
-  S.words[0] = (uint32_t*)(base + o);
-  o += words_bytes(P);
-  S.words[1] = (uint32_t*)(base + o);
-  o += words_bytes(P);
+  S.xch = (uint4*)(base + o);
+  o += sizeof(uint4) * 32 * 5;
+  S.meas = (double*)(base + o);
+  o += align16(sizeof(double) * kMeasStride * sA * sT);
+  S.mcount = (uint16_t*)(base + o);
+  o += align16(sizeof(uint16_t) * sA * sT);
+  S.mlist = (uint16_t*)(base + o);
+  o += align16(sizeof(uint16_t) * sA * sT * sA);
+  S.flags = base + o;
+  o += align16(blockDim.x);
+  S.mbar = (uint64_t*)(base + o);
+  o += 16;
+  S.pf = (double*)(base + o);
+  o += align16(sizeof(double) * 5 * (size_t)P);
   S.cum = (double*)(base + o);
   S.st = S.cum + P;
   return S;
 }
 
+__device__ __forceinline__ Smem carve_dyn(int sA, int sT, int P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return carve(smem_raw, sA, sT, P);
+}
+
 __device__ __forceinline__ const DevConfig& cfg_of(const DevBatch& B, int64_t e) {
   return B.cfgs[B.cfg_of_env ? B.cfg_of_env[e] : 0];
-}
-__device__ __forceinline__ int64_t rec_off(const DevBatch& B, int64_t e) {
-  return B.rec_offset ? B.rec_offset[e] : e * (int64_t)B.cfgs[0].rec_words;
 }
 __device__ __forceinline__ int64_t set_off(const DevBatch& B, int64_t e) {
   return B.set_offset ? B.set_offset[e] : e * (int64_t)(B.cfgs[0].A * B.cfgs[0].T);
@@ -124,119 +140,119 @@ __device__ __forceinline__ int64_t set_off(const DevBatch& B, int64_t e) {
 __device__ __forceinline__ void load_tables(const Smem& S) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) S.tab_log[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
   for (int i = threadIdx.x; i < 64; i += blockDim.x) S.tab_sc[i] = make_double2(kSinCosTab[2 * i], kSinCosTab[2 * i + 1]);
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) S.tab_exp[i] = kExp2Tab[i];
 }
 
-// --------------------------------------------------- serial env prologue ---
-// Environment::scripted_action (env.cpp:511-543) for every agent, on the
-// pre-step state (VecEnv::step_policy computes all actions first, vecenv.cpp:123-124).
-__device__ __noinline__ void scripted_actions(const DevConfig& c, const double* rec, int* act) {
-  const int A = c.A, T = c.T, AT = A * T;
-  const double* ag = rec + c.o_agent;
-  const double* trk = rec + c.o_track;
-  for (int a = 0; a < A; ++a) {
-    const double sx = ag[V_X * A + a], sy = ag[V_Y * A + a], sh = ag[V_HEAD * A + a];
-    const int rud = (int)ag[V_RUDDER * A + a];
-    double gx = sx, gy = sy, best = CUDART_INF;
-    for (int t = 0; t < T; ++t) {
-      const int si = a * T + t;
-      const double ex = trk[K_EX * AT + si], ey = trk[K_EY * AT + si];
-      const double d = norm2(ex - sx, ey - sy);
-      const double penalty = trk[K_EVER * AT + si] != 0.0 ? 0.0 : 1e6;
-      if (d + penalty < best) {
-        best = d + penalty;
-        gx = ex;
-        gy = ey;
-      }
+// The CTA's contiguous env range.
+__device__ __forceinline__ void cta_range(int64_t n, int64_t& lo, int64_t& hi) {
+  const int64_t base = n / gridDim.x, extra = n % gridDim.x, b = blockIdx.x;
+  lo = b * base + (b < extra ? b : extra);
+  hi = lo + base + (b < extra ? 1 : 0);
+}
+
+// ------------------------------------------------ per-env serial phases ---
+// Environment::scripted_action (env.cpp:511-543) on the pre-step state of agent
+// a (only its own pose and tracks are read, so it may run right before a moves).
+__device__ __noinline__ int scripted_action(const DevConfig& c, const Rec& rec, int a) {
+  const int T = c.T;
+  const double sx = AG(V_X, a), sy = AG(V_Y, a), sh = AG(V_HEAD, a);
+  const int rud = (int)AG(V_RUDDER, a);
+  double gx = sx, gy = sy, best = CUDART_INF;
+  for (int t = 0; t < T; ++t) {
+    const int ti = a * c.sT + t;
+    const double ex = TRK(K_EX, ti), ey = TRK(K_EY, ti);
+    const double d = norm2(ex - sx, ey - sy);
+    const double penalty = TRK(K_EVER, ti) != 0.0 ? 0.0 : 1e6;
+    if (d + penalty < best) {
+      best = d + penalty;
+      gx = ex;
+      gy = ey;
     }
-    const double desired = atan2(gy - sy, gx - sx);
-    int best_act = rud;
-    double best_mis = CUDART_INF;
-    for (int i = 0; i < 5; ++i) {
-      if (abs(i - rud) > 1) continue;
-      const double dpsi = c.head_a * (-0.24 + 0.12 * i) + c.head_b;
-      const double mis = fabs(wrap_angle(sh + dpsi - desired));
-      if (mis < best_mis) {
-        best_mis = mis;
-        best_act = i;
-      }
-    }
-    act[a] = best_act;
   }
+  const double desired = atan2(gy - sy, gx - sx);
+  int best_act = rud;
+  double best_mis = CUDART_INF;
+  for (int i = 0; i < 5; ++i) {
+    if (abs(i - rud) > 1) continue;
+    const double dpsi = c.head_a * (-0.24 + 0.12 * i) + c.head_b;
+    const double mis = fabs(wrap_angle(sh + dpsi - desired));
+    if (mis < best_mis) {
+      best_mis = mis;
+      best_act = i;
+    }
+  }
+  return best_act;
 }
 
-// Actions + move_targets + move_agents + measure_ranges + comm decisions, in
-// the reference's env-stream draw order, then the per-set
-// measurement schedule. Thread 0 only.
-__device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t e, int64_t gi,
-                             int mode) {
-  const int A = c.A, T = c.T;
-  double* rec = S.rec;
-  double* ag = rec + c.o_agent;
-  double* tg = rec + c.o_target;
-  double* miss = rec + c.o_miss;
-  double* info = rec + c.o_info;
-  const int AA = A * A;
+// Actions + move_targets + move_agents + measure_ranges + comm decisions for
+// env e, in the reference's env-stream draw order. Writes
+// the ping schedule (horizontal ranges, present and link flags) to scratch.
+__device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B, int64_t e, int64_t gi, int mode) {
+  const Rec rec = rec_of(B, e);
+  const int A = c.A, T = c.T, sA = c.sA, sT = c.sT, AA = sA * sA;
+  double* r2 = B.sched_r2 + e * (int64_t)(sA * sT);
+  uint8_t* present = B.sched_flags + e * (int64_t)(sA * sT + AA);
+  uint8_t* link = present + sA * sT;
   SerialRng rng;
   rng.init(derive_key(B.seed, kTagEnv, (uint64_t)gi, 0), (uint64_t)gi, (uint64_t)rec[R_ENV_POS],
            rec[R_ENV_HAVE_SPARE] != 0.0, rec[R_ENV_SPARE]);
 
-  // actions: VecEnv::step_policy (vecenv.cpp:118-135) or the caller's
-  if (mode == MODE_RANDOM) {
-    SerialRng b;
-    b.init(derive_key(B.seed, kTagBench, (uint64_t)gi, 0), (uint64_t)gi, (uint64_t)rec[R_BENCH_POS], false, 0.0);
-    for (int a = 0; a < A; ++a) {
-      const int rud = (int)ag[V_RUDDER * A + a];
-      int legal[5], nl = 0;
-      for (int q = 0; q < 5; ++q)
-        if (abs(q - rud) <= 1) legal[nl++] = q;
-      S.act[a] = legal[b.uniform_int((uint32_t)nl)];
-    }
-    rec[R_BENCH_POS] = (double)b.pos;
-  } else if (mode == MODE_SCRIPTED) {
-    scripted_actions(c, rec, S.act);
-  } else {
-    for (int a = 0; a < A; ++a) S.act[a] = B.actions[e * B.A_max + a];
-  }
-
   // move_targets (env.cpp:289-304)
   for (int t = 0; t < T; ++t) {
-    if (tg[V_COUNTDOWN * T + t] <= 0.0) {
-      tg[V_CMD * T + t] = wrap_angle(kTwoPi * rng.uniform());
-      tg[V_COUNTDOWN * T + t] = (double)rng.geometric_i32(c.turn_interval);
+    if (TG(V_COUNTDOWN, t) <= 0.0) {
+      TG(V_CMD, t) = wrap_angle(kTwoPi * rng.uniform());
+      TG(V_COUNTDOWN, t) = (double)rng.geometric_i32(c.turn_interval);
     }
-    const double want = wrap_angle(tg[V_CMD * T + t] - tg[V_HEAD * T + t]);
+    const double want = wrap_angle(TG(V_CMD, t) - TG(V_HEAD, t));
     const double mt = c.max_turn;
     const double dpsi = want < -mt ? -mt : (mt < want ? mt : want);
     const double noise = c.head_noise > 0.0 ? c.head_noise * rng.normal() : 0.0;
     // advance_vehicle (kinematics.cpp:42-49)
-    const double h = wrap_angle(tg[V_HEAD * T + t] + dpsi + noise);
-    tg[V_HEAD * T + t] = h;
-    tg[V_X * T + t] += tg[V_SPEED * T + t] * c.dt * cos(h);
-    tg[V_Y * T + t] += tg[V_SPEED * T + t] * c.dt * sin(h);
-    tg[V_COUNTDOWN * T + t] -= 1.0;
+    const double h = wrap_angle(TG(V_HEAD, t) + dpsi + noise);
+    TG(V_HEAD, t) = h;
+    TG(V_X, t) += TG(V_SPEED, t) * c.dt * cos(h);
+    TG(V_Y, t) += TG(V_SPEED, t) * c.dt * sin(h);
+    TG(V_COUNTDOWN, t) -= 1.0;
   }
-  // move_agents (env.cpp:306-316) + step_vehicle (kinematics.cpp:51-56)
+  // actions (VecEnv::step_policy vecenv.cpp:118-135 or the caller's) + move_agents
+  // (env.cpp:306-316, step_vehicle kinematics.cpp:51-56). The bench stream is
+  // separate from the env stream and every action depends only on the agent's
+  // own pre-step state, so choosing each action right before its agent moves
+  // draws exactly the reference's values.
+  SerialRng bench;
+  if (mode == MODE_RANDOM)
+    bench.init(derive_key(B.seed, kTagBench, (uint64_t)gi, 0), (uint64_t)gi, (uint64_t)rec[R_BENCH_POS], false, 0.0);
   for (int a = 0; a < A; ++a) {
-    const int rud = S.act[a];
-    ag[V_RUDDER * A + a] = (double)rud;
-    const double gamma = -0.24 + 0.12 * rud;
+    int act;
+    if (mode == MODE_RANDOM) {
+      const int rud = (int)AG(V_RUDDER, a);
+      const int lo = rud > 0 ? rud - 1 : 0, hi = rud < 4 ? rud + 1 : 4;
+      act = lo + (int)bench.uniform_int((uint32_t)(hi - lo + 1));
+    } else if (mode == MODE_SCRIPTED) {
+      act = scripted_action(c, rec, a);
+    } else {
+      act = B.actions[e * B.A_max + a];
+    }
+    AG(V_RUDDER, a) = (double)act;
+    const double gamma = -0.24 + 0.12 * act;
     double noise = c.head_noise > 0.0 ? c.head_noise * rng.normal() : 0.0;
     if (c.pert_std > 0.0) noise += c.pert_std * rng.normal();
     const double dpsi = c.head_a * gamma + c.head_b;
-    const double h = wrap_angle(ag[V_HEAD * A + a] + dpsi + noise);
-    ag[V_HEAD * A + a] = h;
-    ag[V_X * A + a] += ag[V_SPEED * A + a] * c.dt * cos(h);
-    ag[V_Y * A + a] += ag[V_SPEED * A + a] * c.dt * sin(h);
+    const double h = wrap_angle(AG(V_HEAD, a) + dpsi + noise);
+    AG(V_HEAD, a) = h;
+    AG(V_X, a) += AG(V_SPEED, a) * c.dt * cos(h);
+    AG(V_Y, a) += AG(V_SPEED, a) * c.dt * sin(h);
   }
+  if (mode == MODE_RANDOM) rec[R_BENCH_POS] = (double)bench.pos;
   // measure_ranges (env.cpp:318-347): targets outer, agents inner
   for (int t = 0; t < T; ++t) {
     bool detected = false;
+    const double tx = TG(V_X, t), ty = TG(V_Y, t), tz = TG(V_Z, t);
     for (int a = 0; a < A; ++a) {
-      const int idx = a * T + t;
-      S.present[idx] = 0;
-      const double ax = ag[V_X * A + a], ay = ag[V_Y * A + a], az = ag[V_Z * A + a];
-      const double tz = tg[V_Z * T + t];
-      const double dist3 = norm3(ax - tg[V_X * T + t], ay - tg[V_Y * T + t], az - tz);
+      const int idx = a * sT + t;
+      present[idx] = 0;
+      const double ax = AG(V_X, a), ay = AG(V_Y, a), az = AG(V_Z, a);
+      const double dist3 = norm3(ax - tx, ay - ty, az - tz);
       if (dist3 > c.det_range) continue;
       if (c.drop > 0.0 && rng.uniform() < c.drop) continue;
       double r3 = dist3;
@@ -244,49 +260,283 @@ __device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B,
       r3 = r3 < 0.0 ? 0.0 : r3;
       const double dd = tz - az;
       const double sq = r3 * r3 - dd * dd;  // slant_to_horizontal (tracking.cpp:9-14)
-      double* m = S.meas + kMeasStride * idx;
-      m[0] = ax;
-      m[1] = ay;
-      m[2] = sq <= 0.0 ? 0.0 : sqrt(sq);
-      m[3] = c.sigma_meas;
-      m[4] = 1.0 / c.sigma_meas;
-      S.present[idx] = 1;
+      r2[idx] = sq <= 0.0 ? 0.0 : sqrt(sq);
+      present[idx] = 1;
       detected = true;
     }
-    miss[t] = detected ? 0.0 : miss[t] + 1.0;
+    rec[c.o_miss + t] = detected ? 0.0 : rec[c.o_miss + t] + 1.0;
   }
-  // exchange_comms decisions (env.cpp:365-383)
-  for (int i = 0; i < AA; ++i) info[I_AGE * AA + i] += 1.0;
+  // exchange_comms decisions (env.cpp:365-383); AgentInfo ages first
   for (int r = 0; r < A; ++r)
+    for (int s = 0; s < A; ++s) INFO(I_AGE, r * sA + s) += 1.0;
+  for (int r = 0; r < A; ++r) {
+    const double rx = AG(V_X, r), ry = AG(V_Y, r), rz = AG(V_Z, r);
     for (int s = 0; s < A; ++s) {
-      S.link[r * A + s] = 0;
+      const int k = r * sA + s;
+      link[k] = 0;
       if (s == r) continue;
-      const double sx = ag[V_X * A + s], sy = ag[V_Y * A + s], sz = ag[V_Z * A + s];
-      if (norm3(ag[V_X * A + r] - sx, ag[V_Y * A + r] - sy, ag[V_Z * A + r] - sz) > c.comm_range) continue;
+      const double sx = AG(V_X, s), sy = AG(V_Y, s), sz = AG(V_Z, s);
+      if (norm3(rx - sx, ry - sy, rz - sz) > c.comm_range) continue;
       if (c.drop > 0.0 && rng.uniform() < c.drop) continue;
-      const int k = r * A + s;
-      info[I_X * AA + k] = sx;
-      info[I_Y * AA + k] = sy;
-      info[I_Z * AA + k] = sz;
-      info[I_HEAD * AA + k] = ag[V_HEAD * A + s];
-      info[I_AGE * AA + k] = 0.0;
-      info[I_VALID * AA + k] = 1.0;
-      S.link[k] = 1;
+      INFO(I_X, k) = sx;
+      INFO(I_Y, k) = sy;
+      INFO(I_Z, k) = sz;
+      INFO(I_HEAD, k) = AG(V_HEAD, s);
+      INFO(I_AGE, k) = 0.0;
+      INFO(I_VALID, k) = 1.0;
+      link[k] = 1;
     }
-  // per-set update schedule: own ping first (env.cpp:356-360), then the fused
-  // senders in ascending order (env.cpp:370-392)
-  for (int a = 0; a < A; ++a)
-    for (int t = 0; t < T; ++t) {
-      const int si = a * T + t;
-      int n = 0;
-      if (S.present[si]) S.mlist[si * A + n++] = (uint8_t)si;
-      for (int s = 0; s < A; ++s)
-        if (s != a && S.link[a * A + s] && S.present[s * T + t]) S.mlist[si * A + n++] = (uint8_t)(s * T + t);
-      S.mcount[si] = (uint8_t)n;
-    }
+  }
   rec[R_ENV_POS] = (double)rng.pos;
   rec[R_ENV_HAVE_SPARE] = rng.have_spare ? 1.0 : 0.0;
   rec[R_ENV_SPARE] = rng.spare;
+}
+
+// compute_reward_and_info (env.cpp:473-505) + VecEnv bookkeeping
+// (vecenv.cpp:95-104) + device statistics for env e. Returns done.
+__device__ __noinline__ bool env_epilogue(const DevConfig& c, const DevBatch& B, int64_t e) {
+  const Rec rec = rec_of(B, e);
+  const int A = c.A, T = c.T, Tm = B.T_max;
+  double reward_sum = 0.0, follow_sum = 0.0, err_sum = 0.0, lost_n = 0.0;
+  for (int t = 0; t < T; ++t) {
+    const double tx = TG(V_X, t), ty = TG(V_Y, t);
+    double best_err = CUDART_INF, best_dist = CUDART_INF;
+    for (int a = 0; a < A; ++a) {
+      const int ti = a * c.sT + t;
+      const double d = norm2(TRK(K_EX, ti) - tx, TRK(K_EY, ti) - ty);
+      best_err = d < best_err ? d : best_err;
+    }
+    for (int a = 0; a < A; ++a) {
+      const double d = hypot(AG(V_X, a) - tx, AG(V_Y, a) - ty);
+      best_dist = d < best_dist ? d : best_dist;
+    }
+    const bool lost = rec[c.o_miss + t] >= (double)c.lost_steps;
+    B.track_err[e * Tm + t] = best_err;
+    B.min_dist[e * Tm + t] = best_dist;
+    B.lost[e * Tm + t] = lost ? 1 : 0;
+    // tracking_reward_single (env.cpp:83-90)
+    double rt;
+    if (best_err < c.eps_min) {
+      rt = 1.0;
+    } else if (best_err > c.eps_max) {
+      rt = 0.0;
+    } else {
+      const double tt = (best_err - c.eps_min) / (c.eps_max - c.eps_min);
+      rt = tt >= 1.0 ? 0.0 : exp(-2.0 * tt / (1.0 - tt));
+    }
+    reward_sum += rt;
+    follow_sum += best_dist <= c.d_min ? 1.0 : 0.0;
+    err_sum += best_err;
+    lost_n += lost ? 1.0 : 0.0;
+  }
+  for (int t = T; t < Tm; ++t) {
+    B.track_err[e * Tm + t] = 0.0;
+    B.min_dist[e * Tm + t] = 0.0;
+    B.lost[e * Tm + t] = 0;
+  }
+  bool crash = false;  // crash_check (env.cpp:99-104)
+  for (int i = 0; i + 1 < A && !crash; ++i)
+    for (int j = i + 1; j < A && !crash; ++j)
+      if (norm3(AG(V_X, i) - AG(V_X, j), AG(V_Y, i) - AG(V_Y, j), AG(V_Z, i) - AG(V_Z, j)) < c.d_safe) crash = true;
+  double reward;
+  if (crash)
+    reward = -1.0;
+  else if (c.reward_mode == 0)
+    reward = reward_sum / (double)T;
+  else
+    reward = follow_sum / (double)T;
+  const double step = rec[R_STEP] + 1.0;
+  rec[R_STEP] = step;
+  const bool done = step >= (double)c.horizon;
+  B.rewards[e] = reward;
+  B.dones[e] = done ? 1 : 0;
+  B.collision[e] = crash ? 1 : 0;
+  B.step[e] = (int32_t)step;
+  // statistics (marl.cpp:288-306 accumulators)
+  STAT(0) += 1.0;
+  STAT(1) += reward;
+  STAT(2) += err_sum / (double)T;
+  STAT(5) += crash ? 1.0 : 0.0;
+  STAT(6) += lost_n;
+  rec[R_EP_RETURN] += reward;
+  if (done) {
+    STAT(3) += 1.0;
+    STAT(4) += rec[R_EP_RETURN];
+  }
+  return done;
+}
+
+// Environment::spawn, serial part (env.cpp:155-212, 221-224) for env e.
+// Returns false when the rejection sampling fails (ConfigError in the reference).
+__device__ __noinline__ bool spawn_serial(const DevConfig& c, const DevBatch& B, int64_t e, int64_t gi) {
+  const Rec rec = rec_of(B, e);
+  const int A = c.A, T = c.T, R = c.R, sA = c.sA;
+  SerialRng rng;
+  rng.init(derive_key(B.seed, kTagEnv, (uint64_t)gi, 0), (uint64_t)gi, (uint64_t)rec[R_ENV_POS],
+           rec[R_ENV_HAVE_SPARE] != 0.0, rec[R_ENV_SPARE]);
+  double eps = c.tgt_lo;
+  if (c.tgt_hi > c.tgt_lo) eps = rng.uniform(c.tgt_lo, c.tgt_hi);
+  rec[R_EP_SPEED] = eps;
+  double qx[kMaxEntities], qy[kMaxEntities];
+  bool placed = false;
+  for (int attempt = 0; attempt < 1000 && !placed; ++attempt) {
+    for (int i = 0; i < R; ++i) {
+      const double r = c.disc_r * sqrt(rng.uniform());
+      const double an = kTwoPi * rng.uniform();
+      double sa, ca;
+      sincos(an, &sa, &ca);
+      qx[i] = r * ca;
+      qy[i] = r * sa;
+    }
+    placed = true;
+    for (int i = 0; i + 1 < R && placed; ++i)
+      for (int j = i + 1; j < R && placed; ++j)
+        if (norm2(qx[i] - qx[j], qy[i] - qy[j]) < c.min_sep) placed = false;
+  }
+  if (!placed) {
+    rec[R_ENV_POS] = (double)rng.pos;
+    return false;
+  }
+  for (int a = 0; a < A; ++a) {
+    AG(V_X, a) = qx[a];
+    AG(V_Y, a) = qy[a];
+    AG(V_Z, a) = 0.0;
+    AG(V_HEAD, a) = wrap_angle(kTwoPi * rng.uniform());
+    AG(V_SPEED, a) = c.agent_speed;
+    AG(V_RUDDER, a) = 2.0;
+  }
+  for (int t = 0; t < T; ++t) {
+    const double depth = rng.uniform(c.depth_min, c.depth_max);
+    TG(V_X, t) = qx[A + t];
+    TG(V_Y, t) = qy[A + t];
+    TG(V_Z, t) = depth;
+    const double h = wrap_angle(kTwoPi * rng.uniform());
+    TG(V_HEAD, t) = h;
+    TG(V_SPEED, t) = eps;
+    TG(V_RUDDER, t) = 2.0;
+    TG(V_CMD, t) = h;
+    TG(V_COUNTDOWN, t) = (double)rng.geometric_i32(c.turn_interval);
+  }
+  for (int f = 0; f < I_NFIELD; ++f)
+    for (int r = 0; r < A; ++r)
+      for (int s = 0; s < A; ++s) INFO(f, r * sA + s) = 0.0;
+  for (int t = 0; t < T; ++t) rec[c.o_miss + t] = 0.0;
+  rec[R_STEP] = 0.0;
+  rec[R_EP_RETURN] = 0.0;
+  rec[R_ENV_POS] = (double)rng.pos;
+  rec[R_ENV_HAVE_SPARE] = rng.have_spare ? 1.0 : 0.0;
+  rec[R_ENV_SPARE] = rng.spare;
+  return true;
+}
+
+// ----------------------------------------------------------- outputs ---
+// build_observation (env.cpp:412-453) for (env, agent, row) into the batch
+// layout (vecenv.cpp:47-53); padding rows of mixed fleets are zero.
+__device__ __forceinline__ void token_row(const DevConfig& c, const Rec& rec, int a, int r, double v[12]) {
+#pragma unroll
+  for (int q = 0; q < 12; ++q) v[q] = 0.0;
+  const int A = c.A, R = c.R;
+  if (a >= A || r >= R) return;
+  const double sx = AG(V_X, a), sy = AG(V_Y, a), sz = AG(V_Z, a);
+  if (r < A) {
+    if (r == a) {
+      double sh, ch;
+      sincos(AG(V_HEAD, a), &sh, &ch);
+      v[3] = sh;
+      v[4] = ch;
+      v[5] = AG(V_SPEED, a) / 1.0;
+      v[6] = 1.0;
+      v[9] = 1.0;
+    } else {
+      v[7] = 1.0;
+      const int k = a * c.sA + r;
+      if (INFO(I_VALID, k) != 0.0) {
+        v[0] = (INFO(I_X, k) - sx) / 1000.0;
+        v[1] = (INFO(I_Y, k) - sy) / 1000.0;
+        v[2] = (INFO(I_Z, k) - sz) / 1000.0;
+        double sh, ch;
+        sincos(INFO(I_HEAD, k), &sh, &ch);
+        v[3] = sh;
+        v[4] = ch;
+        v[5] = c.agent_speed / 1.0;
+        v[9] = 1.0;
+        v[10] = INFO(I_AGE, k) / 10.0;
+      }
+    }
+  } else {
+    const int t = r - A, ti = a * c.sT + t;
+    v[8] = 1.0;
+    if (TRK(K_EVER, ti) != 0.0) {
+      v[0] = (TRK(K_EX, ti) - sx) / 1000.0;
+      v[1] = (TRK(K_EY, ti) - sy) / 1000.0;
+      v[2] = (TG(V_Z, t) - sz) / 1000.0;
+      v[9] = 1.0;
+      v[10] = TRK(K_AGE, ti) / 10.0;
+      v[11] = TRK(K_SPREAD, ti) / 100.0;
+    }
+  }
+}
+
+// build_global_state (env.cpp:455-471) row r of env e (vecenv.cpp:55).
+__device__ __forceinline__ void global_row(const DevConfig& c, const Rec& rec, int r, double v[12]) {
+#pragma unroll
+  for (int q = 0; q < 12; ++q) v[q] = 0.0;
+  if (r >= c.R) return;
+  const bool is_agent = r < c.A;
+  const int base = is_agent ? c.o_agent : c.o_target, stride = is_agent ? c.sA : c.sT;
+  const int i = is_agent ? r : r - c.A;
+  v[0] = rec[base + V_X * stride + i] / 1000.0;
+  v[1] = rec[base + V_Y * stride + i] / 1000.0;
+  v[2] = rec[base + V_Z * stride + i] / 1000.0;
+  double sh, ch;
+  sincos(rec[base + V_HEAD * stride + i], &sh, &ch);
+  v[3] = sh;
+  v[4] = ch;
+  v[5] = rec[base + V_SPEED * stride + i] / 1.0;
+  v[is_agent ? 7 : 8] = 1.0;
+  v[9] = 1.0;
+}
+
+// Tokens / global rows / masks (vecenv.cpp:47-67) of envs [e0, e1), one thread
+// per row. `sel` (optional) restricts to envs whose chunk flag has that bit;
+// `final_obs` writes the observation rows into the final_obs buffer only.
+__device__ __noinline__ void write_outputs(const DevBatch& B, int64_t e0, int64_t e1, const uint8_t* flags, int sel,
+                                           bool final_obs) {
+  const int Am = B.A_max, Rm = B.R_max;
+  const int64_t n = e1 - e0;
+  double* obs = final_obs ? B.final_obs : B.obs;
+  for (int64_t p = threadIdx.x; p < n * Am * Rm; p += blockDim.x) {
+    const int64_t le = p / (Am * Rm);
+    if (sel && !(flags[le] & sel)) continue;
+    const int q = (int)(p - le * Am * Rm), a = q / Rm, r = q - (q / Rm) * Rm;
+    const int64_t e = e0 + le;
+    double v[12];
+    token_row(cfg_of(B, e), rec_of(B, e), a, r, v);
+    const int64_t row = (e * Am + a) * Rm + r;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) obs[(int64_t)k * B.obs_rows + row] = v[k];
+  }
+  if (final_obs) return;
+  for (int64_t p = threadIdx.x; p < n * Rm; p += blockDim.x) {
+    const int64_t le = p / Rm;
+    if (sel && !(flags[le] & sel)) continue;
+    const int r = (int)(p - le * Rm);
+    const int64_t e = e0 + le;
+    double v[12];
+    global_row(cfg_of(B, e), rec_of(B, e), r, v);
+    const int64_t row = e * Rm + r;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) B.global[(int64_t)k * B.global_rows + row] = v[k];
+  }
+  for (int64_t p = threadIdx.x; p < n * Am * 5; p += blockDim.x) {
+    const int64_t le = p / (Am * 5);
+    if (sel && !(flags[le] & sel)) continue;
+    const int q = (int)(p - le * Am * 5), a = q / 5, k = q - (q / 5) * 5;
+    const int64_t e = e0 + le;
+    const DevConfig& c = cfg_of(B, e);
+    const Rec rec = rec_of(B, e);
+    B.masks[e * Am * 5 + q] = (a < c.A && abs(k - (int)AG(V_RUDDER, a)) <= 1) ? 1 : 0;
+  }
 }
 
 // -------------------------------------------------- particle-set phases ---
@@ -305,92 +555,32 @@ __device__ __forceinline__ void gen_words(uint32_t* words, uint64_t key, uint64_
   for (int i = threadIdx.x; i < nb; i += blockDim.x) w4[i] = philox(key, stream, b0 + (uint64_t)i);
 }
 
-// 4 consecutive words starting at idx (idx % 4 uniform across the warp).
-__device__ __forceinline__ uint4 lds_words4(const uint32_t* w, int idx) {
-  if ((idx & 3) == 0) return *reinterpret_cast<const uint4*>(w + idx);
-  if ((idx & 1) == 0) {
-    const uint2 a = *reinterpret_cast<const uint2*>(w + idx);
-    const uint2 b = *reinterpret_cast<const uint2*>(w + idx + 2);
-    return make_uint4(a.x, a.y, b.x, b.y);
-  }
-  return make_uint4(w[idx], w[idx + 1], w[idx + 2], w[idx + 3]);
-}
-
-template <int PPT>
-__device__ __forceinline__ void load_set(SetRegs<PPT>& s, const DevBatch& B, size_t base, int k0, int P) {
-  if (PPT == 4 && k0 + 4 <= P && (P & 3) == 0) {
-    const double2* px = reinterpret_cast<const double2*>(B.px + base + k0);
-    const double2* py = reinterpret_cast<const double2*>(B.py + base + k0);
-    const double2* vx = reinterpret_cast<const double2*>(B.vx + base + k0);
-    const double2* vy = reinterpret_cast<const double2*>(B.vy + base + k0);
-    const double2* w = reinterpret_cast<const double2*>(B.w + base + k0);
-    double2 t[10] = {px[0], px[1], py[0], py[1], vx[0], vx[1], vy[0], vy[1], w[0], w[1]};
-    s.px[0] = t[0].x, s.px[1] = t[0].y, s.px[2] = t[1].x, s.px[3] = t[1].y;
-    s.py[0] = t[2].x, s.py[1] = t[2].y, s.py[2] = t[3].x, s.py[3] = t[3].y;
-    s.vx[0] = t[4].x, s.vx[1] = t[4].y, s.vx[2] = t[5].x, s.vx[3] = t[5].y;
-    s.vy[0] = t[6].x, s.vy[1] = t[6].y, s.vy[2] = t[7].x, s.vy[3] = t[7].y;
-    s.w[0] = t[8].x, s.w[1] = t[8].y, s.w[2] = t[9].x, s.w[3] = t[9].y;
-    return;
-  }
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = k0 + j;
-    if (k < P) {
-      s.px[j] = B.px[base + k];
-      s.py[j] = B.py[base + k];
-      s.vx[j] = B.vx[base + k];
-      s.vy[j] = B.vy[base + k];
-      s.w[j] = B.w[base + k];
-    } else {
-      s.px[j] = s.py[j] = s.vx[j] = s.vy[j] = s.w[j] = 0.0;
-    }
-  }
-}
-
-template <int PPT>
-__device__ __forceinline__ void store_set(const SetRegs<PPT>& s, const DevBatch& B, size_t base, int k0, int P) {
-  if (PPT == 4 && k0 + 4 <= P && (P & 3) == 0) {
-    double2* px = reinterpret_cast<double2*>(B.px + base + k0);
-    double2* py = reinterpret_cast<double2*>(B.py + base + k0);
-    double2* vx = reinterpret_cast<double2*>(B.vx + base + k0);
-    double2* vy = reinterpret_cast<double2*>(B.vy + base + k0);
-    double2* w = reinterpret_cast<double2*>(B.w + base + k0);
-    px[0] = make_double2(s.px[0], s.px[1]);
-    px[1] = make_double2(s.px[2], s.px[3]);
-    py[0] = make_double2(s.py[0], s.py[1]);
-    py[1] = make_double2(s.py[2], s.py[3]);
-    vx[0] = make_double2(s.vx[0], s.vx[1]);
-    vx[1] = make_double2(s.vx[2], s.vx[3]);
-    vy[0] = make_double2(s.vy[0], s.vy[1]);
-    vy[1] = make_double2(s.vy[2], s.vy[3]);
-    w[0] = make_double2(s.w[0], s.w[1]);
-    w[1] = make_double2(s.w[2], s.w[3]);
-    return;
-  }
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = k0 + j;
-    if (k < P) {
-      B.px[base + k] = s.px[j];
-      B.py[base + k] = s.py[j];
-      B.vx[base + k] = s.vx[j];
-      B.vy[base + k] = s.vy[j];
-      B.w[base + k] = s.w[j];
-    }
+__device__ __forceinline__ void words_at(uint4 x, uint4 y, int off, uint32_t w[4]) {
+  // 4 consecutive words starting at lane `off` of block x, continuing into y
+  switch (off) {
+    case 0: w[0] = x.x, w[1] = x.y, w[2] = x.z, w[3] = x.w; break;
+    case 1: w[0] = x.y, w[1] = x.z, w[2] = x.w, w[3] = y.x; break;
+    case 2: w[0] = x.z, w[1] = x.w, w[2] = y.x, w[3] = y.y; break;
+    default: w[0] = x.w, w[1] = y.x, w[2] = y.y, w[3] = y.z; break;
   }
 }
 
 // pf::update with one measurement (tracking.cpp:119-143) -- the exact
-// sequential path.
+// sequential path, out of line and working on this thread's particles staged in
+// shared memory (px at st[k], py at st[P+k], w at cum[k]). Returns the reducer
+// parity.
 template <int PPT>
-__device__ __noinline__ void pf_update_seq(SetRegs<PPT>& s, const double* m, int k0, int P, BlockReducer& R) {
+__device__ __noinline__ int pf_update_seq(const double* m, int k0, int P, const double* st, double* wts, double* red,
+                                          int parity) {
+  BlockReducer R{red, parity};
   const double ox = m[0], oy = m[1], r2 = m[2], sig = m[3];
   double ll[PPT];
   double mx = -CUDART_INF;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    if (k0 + j < P) {
-      const double dx = s.px[j] - ox, dy = s.py[j] - oy;
+    const int k = k0 + j;
+    if (k < P) {
+      const double dx = st[k] - ox, dy = st[P + k] - oy;
       const double d = sqrt(dx * dx + dy * dy);
       const double q = (d - r2) / sig;
       ll[j] = 0.0 - 0.5 * (q * q);
@@ -404,34 +594,38 @@ __device__ __noinline__ void pf_update_seq(SetRegs<PPT>& s, const double* m, int
     double acc = 0.0;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      if (k0 + j < P) {
-        s.w[j] = s.w[j] * exp(ll[j] - shift);
-        acc = acc + s.w[j];
+      const int k = k0 + j;
+      if (k < P) {
+        wts[k] = wts[k] * exp(ll[j] - shift);
+        acc = acc + wts[k];
       }
     }
     const double sum = R.sum(acc);
     if (isfinite(sum) && sum > 0.0) {
 #pragma unroll
-      for (int j = 0; j < PPT; ++j) s.w[j] = s.w[j] / sum;
-      return;
+      for (int j = 0; j < PPT; ++j)
+        if (k0 + j < P) wts[k0 + j] = wts[k0 + j] / sum;
+      return R.parity;
     }
   }
   const double inv = 1.0 / (double)P;
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) s.w[j] = k0 + j < P ? inv : 0.0;
+  for (int j = 0; j < PPT; ++j)
+    if (k0 + j < P) wts[k0 + j] = inv;
+  return R.parity;
 }
 
 // pf::estimate (tracking.cpp:180-188) in ONE reduction: moments about the set's
 // previous estimate (cx, cy), mean = c + sum w (p - c), spread^2 = second moment
 // minus the squared shift; exact second pass when that subtraction could lose
 // more than ~1e-11 relative.
-template <int PPT>
+template <int PPT, bool FULL>
 __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, int P, double cx, double cy,
                                                BlockReducer& R) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    if (k0 + j < P) {
+    if (FULL || k0 + j < P) {
       const double dx = s.px[j] - cx, dy = s.py[j] - cy;
       a0 = a0 + s.w[j] * dx;
       a1 = a1 + s.w[j] * dy;
@@ -446,7 +640,7 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
   double acc = 0.0;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    if (k0 + j < P) {
+    if (FULL || k0 + j < P) {
       const double dx = s.px[j] - mx, dy = s.py[j] - my;
       acc = acc + s.w[j] * (dx * dx + dy * dy);
     }
@@ -456,11 +650,10 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
 
 // pf::resample (tracking.cpp:147-170): inclusive scan of w in index order, then
 // output j takes the first particle whose cumulative weight reaches (j + u0)/n,
-// clamped to n - 1 (the reference's monotone two-pointer walk): a binary search
-// for the thread's first output, a forward walk for the rest.
-template <int PPT>
+// clamped to n - 1 (the reference's monotone two-pointer walk).
+template <int PPT, bool FULL>
 __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Smem& S) {
-  const int tid = threadIdx.x, NT = blockDim.x;
+  const int tid = threadIdx.x;
   double* cum = S.cum;
   double* st = S.st;
   double* wsum = S.red + 2 * kRedSlots;
@@ -469,7 +662,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     const int k = k0 + q;
-    if (k < P) {
+    if (FULL || k < P) {
       st[k] = s.px[q];
       st[P + k] = s.py[q];
       st[2 * P + k] = s.vx[q];
@@ -494,11 +687,10 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   const double base = woff + excl;
 #pragma unroll
   for (int q = 0; q < PPT; ++q)
-    if (k0 + q < P) cum[k0 + q] = base + loc[q];
-  (void)NT;
+    if (FULL || k0 + q < P) cum[k0 + q] = base + loc[q];
   __syncthreads();
   const double inv_n = 1.0 / (double)P;
-  if (k0 < P) {
+  if (FULL || k0 < P) {
     const double u = ((double)k0 + u0) * inv_n;
     int a = 0, b = P - 1;
     while (a < b) {
@@ -512,7 +704,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
 #pragma unroll
     for (int q = 0; q < PPT; ++q) {
       const int j = k0 + q;
-      if (j < P) {
+      if (FULL || j < P) {
         const double uj = ((double)j + u0) * inv_n;
         // lower_bound over [i, P-1]: usually i or i+1; otherwise a binary search
         // (a plain forward walk diverges over runs of zero-weight particles)
@@ -541,32 +733,100 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   __syncthreads();
 }
 
+// Issue the TMA prefetch of particle set g (5 fields x P doubles) into S.pf.
+__device__ __forceinline__ void prefetch_set(const DevBatch& B, const Smem& S, int64_t g, int P) {
+  const uint32_t bytes = (uint32_t)(sizeof(double) * P);
+  const size_t off = (size_t)g * P;
+  fence_proxy_async();
+  mbar_expect_tx(S.mbar, 5u * bytes);
+  bulk_g2s(S.pf, B.px + off, bytes, S.mbar);
+  bulk_g2s(S.pf + P, B.py + off, bytes, S.mbar);
+  bulk_g2s(S.pf + 2 * P, B.vx + off, bytes, S.mbar);
+  bulk_g2s(S.pf + 3 * P, B.vy + off, bytes, S.mbar);
+  bulk_g2s(S.pf + 4 * P, B.w + off, bytes, S.mbar);
+}
+
 // filter_step (env.cpp:349-363) + fused comm updates (env.cpp:385-392) +
-// finalize (env.cpp:397-409) for ONE set. `wb` is this set's words buffer; the
-// next set's words (if any) are generated into the other buffer on the way.
-template <int PPT>
-__device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int64_t gi,
-                         int64_t gset, int a, int t, int wb, double* stat) {
-  const int P = c.P, tid = threadIdx.x, A = c.A, T = c.T, AT = A * T;
-  const int si = a * T + t;
+// finalize (env.cpp:397-409) for set (a, t) of env e (global set index gset).
+// FULL (P == blockDim * PPT, P % 4 == 0): the set arrives in S.pf by TMA
+// (phase `tphase`), the Philox blocks are computed in registers and the next
+// set `next` (>= 0) is prefetched right after the set-start barrier.
+template <int PPT, bool FULL>
+__device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, const Rec& rec,
+                         int64_t gi, int64_t gset, int a, int t, uint32_t& tphase, int64_t next) {
+  const int P = c.P, tid = threadIdx.x, T = c.T;
+  const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int ps = a * T + t;     // PF stream id / set within the env (env.cpp:130-133)
+  const int ti = a * c.sT + t;  // track index in the record
   const int k0 = tid * PPT;
-  double* trk = S.rec + c.o_track;
-  uint64_t pos = (uint64_t)trk[K_POS * AT + si];
-  const double ms = trk[K_MAXSPEED * AT + si];
-  const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)si);
+  uint64_t pos = (uint64_t)TRK(K_POS, ti);
+  const double ms = TRK(K_MAXSPEED, ti);
+  const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)ps);
   const size_t base = (size_t)gset * P;
-  const uint32_t* words = S.words[wb];
   const int off = (int)(pos & 3);
+  const bool noise = c.noise_on != 0;
+  const uint64_t u0p = pos + (noise ? 4ull * (uint64_t)P : 0ull);  // resample draw follows predict
 
+  // ---- particles into registers
   SetRegs<PPT> s;
-  load_set<PPT>(s, B, base, k0, P);
-
-  // Next set's words into the other buffer (made visible by this set's barriers).
-  if (si + 1 < AT) {
-    const uint64_t npos = (uint64_t)trk[K_POS * AT + si + 1];
-    gen_words(S.words[wb ^ 1], derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)(si + 1)), (uint64_t)(si + 1),
-              npos, (c.noise_on ? 4ull * (uint64_t)P : 0ull) + 2ull);
+  if (FULL) {
+    mbar_wait(S.mbar, tphase);
+    tphase ^= 1u;
+#pragma unroll
+    for (int q = 0; q < PPT; q += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(S.pf + k0 + q);
+      const double2 y = *reinterpret_cast<const double2*>(S.pf + P + k0 + q);
+      const double2 u = *reinterpret_cast<const double2*>(S.pf + 2 * P + k0 + q);
+      const double2 v = *reinterpret_cast<const double2*>(S.pf + 3 * P + k0 + q);
+      const double2 w = *reinterpret_cast<const double2*>(S.pf + 4 * P + k0 + q);
+      s.px[q] = x.x, s.px[q + 1] = x.y, s.py[q] = y.x, s.py[q + 1] = y.y;
+      s.vx[q] = u.x, s.vx[q + 1] = u.y, s.vy[q] = v.x, s.vy[q + 1] = v.y;
+      s.w[q] = w.x, s.w[q + 1] = w.y;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = k0 + j;
+      s.px[j] = s.py[j] = s.vx[j] = s.vy[j] = s.w[j] = 0.0;
+      if (k < P) {
+        s.px[j] = B.px[base + k];
+        s.py[j] = B.py[base + k];
+        s.vx[j] = B.vx[base + k];
+        s.vy[j] = B.vy[base + k];
+        s.w[j] = B.w[base + k];
+      }
+    }
   }
+
+  // ---- Philox words of fill_normals (tracking.cpp:24-37): particle k needs the
+  // words at pos + s*P + k for segments s = 0..3. FULL: thread t computes the
+  // aligned block (pos/4 + s*P/4 + t) of each segment; a misaligned stream takes
+  // its remaining words from the next lane's block (shuffle) or, for lane 31,
+  // from the next warp's lane 0 / segment s+1 (smem exchange).
+  uint4 blk[4];
+  if (FULL && noise) {
+    const uint64_t b0 = (pos >> 2) + (uint64_t)tid;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) blk[q] = philox(key, (uint64_t)ps, b0 + (uint64_t)q * (uint64_t)(P / 4));
+    if (off != 0 && lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) S.xch[warp * 5 + q] = blk[q];
+      if (warp == 0) S.xch[4] = philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P);
+    }
+  }
+  if (tid == 0) {  // the resample draw, broadcast through smem
+    const uint4 x = philox(key, (uint64_t)ps, u0p >> 2);
+    const int o = (int)(u0p & 3);
+    const uint4 y = o == 3 ? philox(key, (uint64_t)ps, (u0p >> 2) + 1) : x;
+    uint32_t w2[4];
+    words_at(x, y, o, w2);
+    reinterpret_cast<uint32_t*>(S.bc)[0] = w2[0];
+    reinterpret_cast<uint32_t*>(S.bc)[1] = w2[1];
+  }
+  __syncthreads();  // set-start barrier: S.pf consumed, xch / u0 published
+  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
+  const uint64_t u0_lo = reinterpret_cast<const uint32_t*>(S.bc)[0];
+  const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
 
   // ---- pf::predict (tracking.cpp:94-117)
 #pragma unroll
@@ -574,37 +834,35 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     s.px[j] = s.px[j] + s.vx[j] * c.dt;
     s.py[j] = s.py[j] + s.vy[j] * c.dt;
   }
-  if (c.noise_on) {
-    const float two_pi_f = 2.0f * 3.14159265358979323846f;
-    // fill_normals: pair i uses u1 = word(pos + i), u2 = word(pos + 2P + i);
-    // particle k takes cos of pairs k and P+k, sin of pairs k and P+k.
-    uint4 W[4];
-    if (PPT == 4 && k0 + 4 <= P) {
+  if (noise) {
+    uint32_t W[4][4];  // [segment][particle]
+    if (FULL) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) W[q] = lds_words4(words, off + q * P + k0);
+      for (int q = 0; q < 4; ++q) {
+        uint4 nb;
+        nb.x = __shfl_down_sync(0xffffffffu, blk[q].x, 1);
+        nb.y = __shfl_down_sync(0xffffffffu, blk[q].y, 1);
+        nb.z = __shfl_down_sync(0xffffffffu, blk[q].z, 1);
+        if (off != 0 && lane == 31) nb = warp + 1 < nw ? S.xch[(warp + 1) * 5 + q] : S.xch[q + 1];
+        words_at(blk[q], nb, off, W[q]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < PPT; ++j)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          W[q][j] = k0 + j < P ? word_at(key, (uint64_t)ps, pos + (uint64_t)q * (uint64_t)P + (uint64_t)(k0 + j)) : 0u;
     }
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const int k = k0 + j;
-      if (k < P) {
-        uint32_t w1a, w1b, w2a, w2b;
-        if (PPT == 4 && k0 + 4 <= P) {
-          w1a = lane_of(W[0], j);
-          w1b = lane_of(W[1], j);
-          w2a = lane_of(W[2], j);
-          w2b = lane_of(W[3], j);
-        } else {
-          w1a = words[off + k];
-          w1b = words[off + P + k];
-          w2a = words[off + 2 * P + k];
-          w2b = words[off + 3 * P + k];
-        }
+      if (FULL || k0 + j < P) {
+        // pair k: u1 = word(pos+k), u2 = word(pos+2P+k); pair P+k: segments 1, 3
         float zpx, zvx, zpy, zvy;  // out[k], out[2P+k] / out[P+k], out[3P+k]
-        bool ok = box_muller_fast(w1a, w2a, S.tab_log, S.tab_sc, zpx, zvx);
-        ok &= box_muller_fast(w1b, w2b, S.tab_log, S.tab_sc, zpy, zvy);
+        bool ok = box_muller_fast(W[0][j], W[2][j], S.tab_log, S.tab_sc, zpx, zvx);
+        ok &= box_muller_fast(W[1][j], W[3][j], S.tab_log, S.tab_sc, zpy, zvy);
         if (!ok) {  // an uncertain rounding (p ~ 1e-4 per particle): exact fp64 libm path
-          box_muller_slow(w1a, w2a, zpx, zvx);
-          box_muller_slow(w1b, w2b, zpy, zvy);
+          box_muller_slow(W[0][j], W[2][j], zpx, zvx);
+          box_muller_slow(W[1][j], W[3][j], zpy, zvy);
         }
         s.px[j] = s.px[j] + c.pn * (double)zpx;
         s.py[j] = s.py[j] + c.pn * (double)zpy;
@@ -612,6 +870,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         s.vy[j] = s.vy[j] + c.vn * (double)zvy;
       }
     }
+    pos += 4ull * (uint64_t)P;
   }
   if (ms > 0.0) {
 #pragma unroll
@@ -622,12 +881,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       s.vy[j] = s.vy[j] * f;
     }
   }
-  const int u0_idx = off + (c.noise_on ? 4 * P : 0);  // resample draw follows predict's 4P
-  if (c.noise_on) pos += 4ull * (uint64_t)P;
 
   // ---- range updates: own ping, then fused senders (env.cpp:356-360, 385-392)
-  const int nm = S.mcount[si];
-  const uint8_t* ml = S.mlist + si * A;
+  const int nm = S.mcount[ti];
+  const uint16_t* ml = S.mlist + ti * c.sA;
   bool have_ess = false;
   double ess = 0.0;
   bool exact = nm > kMaxMerged || B.force_exact;
@@ -645,7 +902,6 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll
     for (int q = 0; q < PPT; ++q) L[q] = 0.0;
     double* mb = R.buf();  // per-stage warp maxima, [stage * 32 + warp]
-    const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
 #pragma unroll 1
     for (int j = 0; j < nm; ++j) {
       const double* m = S.meas + kMeasStride * ml[j];
@@ -653,7 +909,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       double mj = -CUDART_INF;
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
-        if (k0 + q < P) {
+        if (FULL || k0 + q < P) {
           const double dx = s.px[q] - ox, dy = s.py[q] - oy;
           const double d = sqrt(dx * dx + dy * dy);
           const double qv = div_rcp(d - r2, sig, rsig);
@@ -673,10 +929,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     double shift = 0.0;  // sum_j s_j, in stage order
 #pragma unroll 1
     for (int j = 0; j < nm; ++j) {
-      double sj = lane < nw ? mb[j * 32 + lane] : -CUDART_INF;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double u = __shfl_xor_sync(0xffffffffu, sj, o);
+      double sj = -CUDART_INF;
+      for (int v = 0; v < nw; ++v) {
+        const double u = mb[j * 32 + v];
         sj = u > sj ? u : sj;
       }
       shift = j == 0 ? sj : shift + sj;
@@ -688,8 +943,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         e[q] = 0.0;
-        if (k0 + q < P) {
-          e[q] = s.w[q] * exp(L[q] - shift);
+        if (FULL || k0 + q < P) {
+          e[q] = s.w[q] * exp_neg(L[q] - shift, S.tab_exp);
           ls = ls + e[q];
           lq = lq + e[q] * e[q];
           lm = e[q] > lm ? e[q] : lm;
@@ -709,16 +964,31 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         exact = true;
       }
     }
-    if (exact && tid == 0) stat[2] += 1.0;
+    if (exact && tid == 0) STAT(9) += 1.0;
   }
-  if (exact) {
-    for (int j = 0; j < nm; ++j) pf_update_seq<PPT>(s, S.meas + kMeasStride * ml[j], k0, P, R);
+  if (exact && nm > 0) {
+#pragma unroll
+    for (int q = 0; q < PPT; ++q)
+      if (FULL || k0 + q < P) {
+        S.st[k0 + q] = s.px[q];
+        S.st[P + k0 + q] = s.py[q];
+        S.cum[k0 + q] = s.w[q];
+      }
+    for (int j = 0; j < nm; ++j)
+      R.parity = pf_update_seq<PPT>(S.meas + kMeasStride * ml[j], k0, P, S.st, S.cum, R.red, R.parity);
+#pragma unroll
+    for (int q = 0; q < PPT; ++q)
+      if (FULL || k0 + q < P) s.w[q] = S.cum[k0 + q];
+    __syncthreads();  // the staging area is reused by the resample
   }
   const bool fresh = nm > 0;
 
-  // ---- pf::maybe_resample (tracking.cpp:172-178)
+  // ---- pf::maybe_resample (tracking.cpp:172-178). With no update this step the
+  // weights are the ones last step's maybe_resample already vetted (ESS >= P/2),
+  // so the reference's recomputation cannot resample: skipped unless the state
+  // was injected.
   bool resampled = false;
-  const bool ess_known_ok = nm == 0 && trk[K_ESSOK * AT + si] != 0.0;
+  const bool ess_known_ok = nm == 0 && TRK(K_ESSOK, ti) != 0.0;
   if (!ess_known_ok) {
     if (!have_ess) {
       double w2 = 0.0;
@@ -727,47 +997,96 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       ess = 1.0 / R.sum(w2);
     }
     if (ess < (double)P / 2.0) {
-      const uint64_t lo = words[u0_idx], hi = words[u0_idx + 1];
-      const double u0 = (double)(((hi << 32) | lo) >> 11) * 0x1.0p-53;
+      const double u0 = (double)(((u0_hi << 32) | u0_lo) >> 11) * 0x1.0p-53;
       pos += 2;
-      pf_resample<PPT>(s, k0, P, u0, S);
+      pf_resample<PPT, FULL>(s, k0, P, u0, S);
       resampled = true;
     }
   }
 
   if (B.trace_env == gi - B.env_index_offset && tid == 0)
     printf("[trace env %lld set %d] nm=%d exact=%d have_ess=%d ess=%.17g resampled=%d pos=%llu\n",
-           (long long)(gi - B.env_index_offset), si, nm, (int)exact, (int)have_ess, ess, (int)resampled,
+           (long long)(gi - B.env_index_offset), ps, nm, (int)exact, (int)have_ess, ess, (int)resampled,
            (unsigned long long)pos);
 
   // ---- estimate (env.cpp:403-407)
-  const double3 est = pf_estimate<PPT>(s, k0, P, trk[K_EX * AT + si], trk[K_EY * AT + si], R);
-  store_set<PPT>(s, B, base, k0, P);
+  const double3 est = pf_estimate<PPT, FULL>(s, k0, P, TRK(K_EX, ti), TRK(K_EY, ti), R);
+  if (FULL) {
+#pragma unroll
+    for (int q = 0; q < PPT; q += 2) {
+      *reinterpret_cast<double2*>(B.px + base + k0 + q) = make_double2(s.px[q], s.px[q + 1]);
+      *reinterpret_cast<double2*>(B.py + base + k0 + q) = make_double2(s.py[q], s.py[q + 1]);
+      *reinterpret_cast<double2*>(B.vx + base + k0 + q) = make_double2(s.vx[q], s.vx[q + 1]);
+      *reinterpret_cast<double2*>(B.vy + base + k0 + q) = make_double2(s.vy[q], s.vy[q + 1]);
+      *reinterpret_cast<double2*>(B.w + base + k0 + q) = make_double2(s.w[q], s.w[q + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = k0 + j;
+      if (k < P) {
+        B.px[base + k] = s.px[j];
+        B.py[base + k] = s.py[j];
+        B.vx[base + k] = s.vx[j];
+        B.vy[base + k] = s.vy[j];
+        B.w[base + k] = s.w[j];
+      }
+    }
+  }
   if (tid == 0) {
-    trk[K_EX * AT + si] = est.x;
-    trk[K_EY * AT + si] = est.y;
-    trk[K_SPREAD * AT + si] = est.z;
-    trk[K_AGE * AT + si] = fresh ? 0.0 : trk[K_AGE * AT + si] + 1.0;
-    trk[K_EVER * AT + si] = (trk[K_EVER * AT + si] != 0.0 || fresh) ? 1.0 : 0.0;
-    trk[K_POS * AT + si] = (double)pos;
-    trk[K_ESSOK * AT + si] = 1.0;  // maybe_resample ran: ESS >= P/2 or weights uniform
-    stat[0] += (double)nm;
-    stat[1] += resampled ? 1.0 : 0.0;
+    TRK(K_EX, ti) = est.x;
+    TRK(K_EY, ti) = est.y;
+    TRK(K_SPREAD, ti) = est.z;
+    TRK(K_AGE, ti) = fresh ? 0.0 : TRK(K_AGE, ti) + 1.0;
+    TRK(K_EVER, ti) = (TRK(K_EVER, ti) != 0.0 || fresh) ? 1.0 : 0.0;
+    TRK(K_POS, ti) = (double)pos;
+    TRK(K_ESSOK, ti) = 1.0;  // maybe_resample ran: ESS >= P/2 or weights uniform
+    STAT(7) += (double)nm;
+    STAT(8) += resampled ? 1.0 : 0.0;
+  }
+}
+
+// Stage env e's config and ping schedule for the particle phase: measurement
+// rows and the per-set update lists (own ping, then senders in ascending order).
+// Caller syncs.
+__device__ __forceinline__ void stage_env(const DevConfig& cg, const DevBatch& B, const Smem& S, const Rec& rec,
+                                         int64_t e) {
+  const DevConfig& c = cg;
+  const int A = c.A, T = c.T, sA = c.sA, sT = c.sT;
+  const double* r2 = B.sched_r2 + e * (int64_t)(sA * sT);
+  const uint8_t* present = B.sched_flags + e * (int64_t)(sA * sT + sA * sA);
+  const uint8_t* link = present + sA * sT;
+  for (int i = threadIdx.x; i < (int)(sizeof(DevConfig) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(S.cfg)[i] = reinterpret_cast<const uint32_t*>(&cg)[i];
+  for (int i = threadIdx.x; i < A * T; i += blockDim.x) {
+    const int a = i / T, t = i - (i / T) * T, ti = a * sT + t;
+    double* m = S.meas + kMeasStride * ti;
+    m[0] = AG(V_X, a);
+    m[1] = AG(V_Y, a);
+    m[2] = r2[ti];
+    m[3] = c.sigma_meas;
+    m[4] = 1.0 / c.sigma_meas;
+    int n = 0;
+    uint16_t* ml = S.mlist + ti * sA;
+    if (present[ti]) ml[n++] = (uint16_t)ti;
+    for (int s = 0; s < A; ++s)
+      if (s != a && link[a * sA + s] && present[s * sT + t]) ml[n++] = (uint16_t)(s * sT + t);
+    S.mcount[ti] = (uint16_t)n;
   }
 }
 
 // pf::reinit (tracking.cpp:76-92) + estimate for one set (spawn, env.cpp:214-220).
 template <int PPT>
-__device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int64_t gi,
-                           int64_t gset, int si, double cx, double cy, double vmax) {
-  const int P = c.P, tid = threadIdx.x, AT = c.A * c.T;
+__device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, const Rec& rec,
+                           int64_t gi, int64_t gset, int a, int t, double cx, double cy, double vmax) {
+  const int P = c.P, tid = threadIdx.x;
+  const int ps = a * c.T + t, ti = a * c.sT + t;
   const int k0 = tid * PPT;
-  double* trk = S.rec + c.o_track;
-  uint64_t pos = (uint64_t)trk[K_POS * AT + si];
-  const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)si);
+  uint64_t pos = (uint64_t)TRK(K_POS, ti);
+  const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)ps);
   uint32_t* words = reinterpret_cast<uint32_t*>(S.cum);  // the resample area
   __syncthreads();  // that area may still be read by the previous phase
-  gen_words(words, key, (uint64_t)si, pos, 8ull * (uint64_t)P);
+  gen_words(words, key, (uint64_t)ps, pos, 8ull * (uint64_t)P);
   __syncthreads();
   const int off = (int)(pos & 3);
   const double inv = 1.0 / (double)P;
@@ -799,406 +1118,210 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
     }
   }
   pos += 8ull * (uint64_t)P;
-  const double3 est = pf_estimate<PPT>(s, k0, P, cx, cy, R);
-  store_set<PPT>(s, B, (size_t)gset * P, k0, P);
+  const double3 est = pf_estimate<PPT, false>(s, k0, P, cx, cy, R);
+  const size_t base = (size_t)gset * P;
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    const int k = k0 + j;
+    if (k < P) {
+      B.px[base + k] = s.px[j];
+      B.py[base + k] = s.py[j];
+      B.vx[base + k] = s.vx[j];
+      B.vy[base + k] = s.vy[j];
+      B.w[base + k] = s.w[j];
+    }
+  }
   if (tid == 0) {
-    trk[K_EX * AT + si] = est.x;
-    trk[K_EY * AT + si] = est.y;
-    trk[K_SPREAD * AT + si] = est.z;
-    trk[K_AGE * AT + si] = 0.0;
-    trk[K_EVER * AT + si] = 0.0;
-    trk[K_POS * AT + si] = (double)pos;
-    trk[K_MAXSPEED * AT + si] = vmax;
-    trk[K_ESSOK * AT + si] = 1.0;
+    TRK(K_EX, ti) = est.x;
+    TRK(K_EY, ti) = est.y;
+    TRK(K_SPREAD, ti) = est.z;
+    TRK(K_AGE, ti) = 0.0;
+    TRK(K_EVER, ti) = 0.0;
+    TRK(K_POS, ti) = (double)pos;
+    TRK(K_MAXSPEED, ti) = vmax;
+    TRK(K_ESSOK, ti) = 1.0;
   }
   __syncthreads();
 }
 
-// ------------------------------------------------------------- spawn ---
-// Environment::spawn, serial part (env.cpp:155-212, 221-224). Thread 0 only.
-// Returns false when the rejection sampling fails (ConfigError in the reference).
-__device__ __noinline__ bool spawn_serial(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t gi) {
-  const int A = c.A, T = c.T, R = c.R, AA = A * A;
-  double* rec = S.rec;
-  double* ag = rec + c.o_agent;
-  double* tg = rec + c.o_target;
-  SerialRng rng;
-  rng.init(derive_key(B.seed, kTagEnv, (uint64_t)gi, 0), (uint64_t)gi, (uint64_t)rec[R_ENV_POS],
-           rec[R_ENV_HAVE_SPARE] != 0.0, rec[R_ENV_SPARE]);
-  double eps = c.tgt_lo;
-  if (c.tgt_hi > c.tgt_lo) eps = rng.uniform(c.tgt_lo, c.tgt_hi);
-  rec[R_EP_SPEED] = eps;
-  double* qx = S.qxy;
-  double* qy = S.qxy + R;
-  bool placed = false;
-  for (int attempt = 0; attempt < 1000 && !placed; ++attempt) {
-    for (int i = 0; i < R; ++i) {
-      const double r = c.disc_r * sqrt(rng.uniform());
-      const double an = kTwoPi * rng.uniform();
-      double sa, ca;
-      sincos(an, &sa, &ca);
-      qx[i] = r * ca;
-      qy[i] = r * sa;
-    }
-    placed = true;
-    for (int i = 0; i + 1 < R && placed; ++i)
-      for (int j = i + 1; j < R && placed; ++j)
-        if (norm2(qx[i] - qx[j], qy[i] - qy[j]) < c.min_sep) placed = false;
-  }
-  if (!placed) {
-    rec[R_ENV_POS] = (double)rng.pos;
-    return false;
-  }
-  for (int a = 0; a < A; ++a) {
-    ag[V_X * A + a] = qx[a];
-    ag[V_Y * A + a] = qy[a];
-    ag[V_Z * A + a] = 0.0;
-    ag[V_HEAD * A + a] = wrap_angle(kTwoPi * rng.uniform());
-    ag[V_SPEED * A + a] = c.agent_speed;
-    ag[V_RUDDER * A + a] = 2.0;
-  }
-  for (int t = 0; t < T; ++t) {
-    const double depth = rng.uniform(c.depth_min, c.depth_max);
-    tg[V_X * T + t] = qx[A + t];
-    tg[V_Y * T + t] = qy[A + t];
-    tg[V_Z * T + t] = depth;
-    const double h = wrap_angle(kTwoPi * rng.uniform());
-    tg[V_HEAD * T + t] = h;
-    tg[V_SPEED * T + t] = eps;
-    tg[V_RUDDER * T + t] = 2.0;
-    tg[V_CMD * T + t] = h;
-    tg[V_COUNTDOWN * T + t] = (double)rng.geometric_i32(c.turn_interval);
-  }
-  double* info = rec + c.o_info;
-  for (int f = 0; f < I_NFIELD; ++f)
-    for (int i = 0; i < AA; ++i) info[f * AA + i] = 0.0;
-  for (int t = 0; t < T; ++t) rec[c.o_miss + t] = 0.0;
-  rec[R_STEP] = 0.0;
-  rec[R_EP_RETURN] = 0.0;
-  rec[R_ENV_POS] = (double)rng.pos;
-  rec[R_ENV_HAVE_SPARE] = rng.have_spare ? 1.0 : 0.0;
-  rec[R_ENV_SPARE] = rng.spare;
-  return true;
-}
-
-// Full spawn: serial part + every set's re-init. All threads. Returns false on
-// spawn failure (CTA-uniform).
+// Re-init every set of the chunk's envs flagged kChunkFlagSpawned (out of line:
+// works on the global copy of the batch descriptor and the dynamic smem).
 template <int PPT>
-__device__ __noinline__ bool spawn_env(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int64_t e,
-                          int64_t gi) {
-  if (threadIdx.x == 0) S.bc[8] = spawn_serial(c, B, S, gi) ? 1.0 : 0.0;
-  __syncthreads();
-  if (S.bc[8] == 0.0) return false;
-  const int A = c.A, T = c.T;
-  const double vmax = c.speed_margin * S.rec[R_EP_SPEED];
-  const int64_t so = set_off(B, e);
-  for (int a = 0; a < A; ++a) {
-    const double cx = S.rec[c.o_agent + V_X * A + a], cy = S.rec[c.o_agent + V_Y * A + a];
-    for (int t = 0; t < T; ++t) reinit_set<PPT>(c, B, S, R, gi, so + a * T + t, a * T + t, cx, cy, vmax);
-  }
-  return true;
-}
-
-// --------------------------------------------------------- outputs ---
-// build_observation (env.cpp:412-453) / build_global_state (env.cpp:455-471) for
-// env e into the batch layout (vecenv.cpp:47-56), plus masks (vecenv.cpp:58-67).
-__device__ __noinline__ void write_tokens(const DevConfig& c, const DevBatch& B, const double* rec, int64_t e, double* obs,
-                             bool with_global, bool with_masks) {
-  const int A = c.A, T = c.T, R = c.R, Am = B.A_max, Rm = B.R_max, AA = A * A, AT = A * T;
-  const double* ag = rec + c.o_agent;
-  const double* tg = rec + c.o_target;
-  const double* info = rec + c.o_info;
-  const double* trk = rec + c.o_track;
-  for (int p = threadIdx.x; p < Am * Rm; p += blockDim.x) {
-    const int a = p / Rm, r = p - (p / Rm) * Rm;
-    double v[12];
-#pragma unroll
-    for (int q = 0; q < 12; ++q) v[q] = 0.0;
-    if (a < A && r < R) {
-      const double sx = ag[V_X * A + a], sy = ag[V_Y * A + a], sz = ag[V_Z * A + a];
-      if (r < A) {
-        if (r == a) {
-          double sh, ch;
-          sincos(ag[V_HEAD * A + a], &sh, &ch);
-          v[3] = sh;
-          v[4] = ch;
-          v[5] = ag[V_SPEED * A + a] / 1.0;
-          v[6] = 1.0;
-          v[9] = 1.0;
-        } else {
-          v[7] = 1.0;
-          const int k = a * A + r;
-          if (info[I_VALID * AA + k] != 0.0) {
-            v[0] = (info[I_X * AA + k] - sx) / 1000.0;
-            v[1] = (info[I_Y * AA + k] - sy) / 1000.0;
-            v[2] = (info[I_Z * AA + k] - sz) / 1000.0;
-            double sh, ch;
-            sincos(info[I_HEAD * AA + k], &sh, &ch);
-            v[3] = sh;
-            v[4] = ch;
-            v[5] = c.agent_speed / 1.0;
-            v[9] = 1.0;
-            v[10] = info[I_AGE * AA + k] / 10.0;
-          }
-        }
-      } else {
-        const int t = r - A, si = a * T + t;
-        v[8] = 1.0;
-        if (trk[K_EVER * AT + si] != 0.0) {
-          v[0] = (trk[K_EX * AT + si] - sx) / 1000.0;
-          v[1] = (trk[K_EY * AT + si] - sy) / 1000.0;
-          v[2] = (tg[V_Z * T + t] - sz) / 1000.0;
-          v[9] = 1.0;
-          v[10] = trk[K_AGE * AT + si] / 10.0;
-          v[11] = trk[K_SPREAD * AT + si] / 100.0;
-        }
-      }
-    }
-    const int64_t row = (e * Am + a) * Rm + r;
-#pragma unroll
-    for (int q = 0; q < 12; ++q) obs[(int64_t)q * B.obs_rows + row] = v[q];
-  }
-  if (with_global) {
-    for (int r = threadIdx.x; r < Rm; r += blockDim.x) {
-      double v[12];
-#pragma unroll
-      for (int q = 0; q < 12; ++q) v[q] = 0.0;
-      if (r < R) {
-        const bool is_agent = r < A;
-        const double* src = is_agent ? ag : tg;
-        const int n = is_agent ? A : T, i = is_agent ? r : r - A;
-        v[0] = src[V_X * n + i] / 1000.0;
-        v[1] = src[V_Y * n + i] / 1000.0;
-        v[2] = src[V_Z * n + i] / 1000.0;
-        double sh, ch;
-        sincos(src[V_HEAD * n + i], &sh, &ch);
-        v[3] = sh;
-        v[4] = ch;
-        v[5] = src[V_SPEED * n + i] / 1.0;
-        v[is_agent ? 7 : 8] = 1.0;
-        v[9] = 1.0;
-      }
-      const int64_t row = e * Rm + r;
-#pragma unroll
-      for (int q = 0; q < 12; ++q) B.global[(int64_t)q * B.global_rows + row] = v[q];
+__device__ __noinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t e1) {
+  const Smem S = carve_dyn(B.cfgs[0].sA, B.cfgs[0].sT, B.P);
+  BlockReducer R{S.red, 0};
+  for (int64_t e = e0; e < e1; ++e) {
+    if (!(S.flags[e - e0] & kChunkFlagSpawned)) continue;
+    const DevConfig& c = cfg_of(B, e);
+    const Rec rec = rec_of(B, e);
+    const int64_t gi = B.env_index_offset + e;
+    const double vmax = c.speed_margin * rec[R_EP_SPEED];
+    const int64_t so = set_off(B, e);
+    for (int a = 0; a < c.A; ++a) {
+      const double cx = AG(V_X, a), cy = AG(V_Y, a);
+      for (int t = 0; t < c.T; ++t) reinit_set<PPT>(c, B, S, R, rec, gi, so + a * c.T + t, a, t, cx, cy, vmax);
     }
   }
-  if (with_masks) {
-    for (int p = threadIdx.x; p < Am * 5; p += blockDim.x) {
-      const int a = p / 5, k = p - (p / 5) * 5;
-      uint8_t m = 0;
-      if (a < A) m = abs(k - (int)ag[V_RUDDER * A + a]) <= 1 ? 1 : 0;
-      B.masks[e * Am * 5 + p] = m;
-    }
-  }
-}
-
-// compute_reward_and_info (env.cpp:473-505) + VecEnv bookkeeping
-// (vecenv.cpp:95-104) + device statistics. Thread 0 only. Returns done.
-__device__ __noinline__ bool env_epilogue(const DevConfig& c, const DevBatch& B, const Smem& S, int64_t e) {
-  const int A = c.A, T = c.T, AT = A * T, Tm = B.T_max;
-  double* rec = S.rec;
-  const double* ag = rec + c.o_agent;
-  const double* tg = rec + c.o_target;
-  const double* trk = rec + c.o_track;
-  double reward_sum = 0.0, follow_sum = 0.0, err_sum = 0.0, lost_n = 0.0;
-  for (int t = 0; t < T; ++t) {
-    const double tx = tg[V_X * T + t], ty = tg[V_Y * T + t];
-    double best_err = CUDART_INF, best_dist = CUDART_INF;
-    for (int a = 0; a < A; ++a) {
-      const int si = a * T + t;
-      const double d = norm2(trk[K_EX * AT + si] - tx, trk[K_EY * AT + si] - ty);
-      best_err = d < best_err ? d : best_err;
-    }
-    for (int a = 0; a < A; ++a) {
-      const double d = hypot(ag[V_X * A + a] - tx, ag[V_Y * A + a] - ty);
-      best_dist = d < best_dist ? d : best_dist;
-    }
-    const bool lost = rec[c.o_miss + t] >= (double)c.lost_steps;
-    B.track_err[e * Tm + t] = best_err;
-    B.min_dist[e * Tm + t] = best_dist;
-    B.lost[e * Tm + t] = lost ? 1 : 0;
-    // tracking_reward_single (env.cpp:83-90)
-    double rt;
-    if (best_err < c.eps_min) {
-      rt = 1.0;
-    } else if (best_err > c.eps_max) {
-      rt = 0.0;
-    } else {
-      const double tt = (best_err - c.eps_min) / (c.eps_max - c.eps_min);
-      rt = tt >= 1.0 ? 0.0 : exp(-2.0 * tt / (1.0 - tt));
-    }
-    reward_sum += rt;
-    follow_sum += best_dist <= c.d_min ? 1.0 : 0.0;
-    err_sum += best_err;
-    lost_n += lost ? 1.0 : 0.0;
-  }
-  for (int t = T; t < Tm; ++t) {
-    B.track_err[e * Tm + t] = 0.0;
-    B.min_dist[e * Tm + t] = 0.0;
-    B.lost[e * Tm + t] = 0;
-  }
-  bool crash = false;  // crash_check (env.cpp:99-104)
-  for (int i = 0; i + 1 < A && !crash; ++i)
-    for (int j = i + 1; j < A && !crash; ++j)
-      if (norm3(ag[V_X * A + i] - ag[V_X * A + j], ag[V_Y * A + i] - ag[V_Y * A + j],
-                ag[V_Z * A + i] - ag[V_Z * A + j]) < c.d_safe)
-        crash = true;
-  double reward;
-  if (crash)
-    reward = -1.0;
-  else if (c.reward_mode == 0)
-    reward = reward_sum / (double)T;
-  else
-    reward = follow_sum / (double)T;
-  const double step = rec[R_STEP] + 1.0;
-  rec[R_STEP] = step;
-  const bool done = step >= (double)c.horizon;
-  B.rewards[e] = reward;
-  B.dones[e] = done ? 1 : 0;
-  B.collision[e] = crash ? 1 : 0;
-  // statistics (marl.cpp:288-306 accumulators)
-  double* st = rec + c.o_stats;
-  st[0] += 1.0;
-  st[1] += reward;
-  st[2] += err_sum / (double)T;
-  st[5] += crash ? 1.0 : 0.0;
-  st[6] += lost_n;
-  rec[R_EP_RETURN] += reward;
-  if (done) {
-    st[3] += 1.0;
-    st[4] += rec[R_EP_RETURN];
-  }
-  return done;
-}
-
-__device__ __forceinline__ void copy_rec(double* dst, const double* src, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
 // ================================================================ kernels ===
-// The fused step: one CTA per env.
 #ifndef UT_STEP_MIN_BLOCKS
 #define UT_STEP_MIN_BLOCKS 2
 #endif
-template <int PPT>
+
+// The fused step.
+template <int PPT, bool FULL>
 __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t e = blockIdx.x;
-  const DevConfig& c = cfg_of(B, e);
-  const Smem S = carve(smem_raw, c.rec_words, c.A, c.T, c.P);
+  const Smem S = carve(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT, B.P);
+  const DevBatch& Bg = *B.self;  // cold paths read the global copy
   BlockReducer R{S.red, 0};
-  const int64_t gi = B.env_index_offset + e;
-  double* grec = B.rec + rec_off(B, e);
-  const long long tc0 = clock64();
   load_tables(S);
-  copy_rec(S.rec, grec, c.rec_words);
+  if (FULL && threadIdx.x == 0) mbar_init(S.mbar, 1);
+  int64_t lo, hi;
+  cta_range(B.n_envs, lo, hi);
+  const int64_t set_end = hi < B.n_envs ? set_off(B, hi) : set_off(B, hi - 1) + cfg_of(B, hi - 1).A * cfg_of(B, hi - 1).T;
   __syncthreads();
-  if (threadIdx.x == 0) env_prologue(c, B, S, e, gi, mode);
-  // first set's words, generated while thread 0 runs the prologue
-  {
-    const int AT = c.A * c.T;
-    const uint64_t pos0 = (uint64_t)S.rec[c.o_track + K_POS * AT];
-    gen_words(S.words[0], derive_key(B.seed, kTagPf, (uint64_t)gi, 0), 0, pos0,
-              (c.noise_on ? 4ull * (uint64_t)c.P : 0ull) + 2ull);
-  }
-  __syncthreads();
-
-  const long long tc1 = clock64();
-
-  const int64_t so = set_off(B, e);
-  double stat[3] = {0.0, 0.0, 0.0};
-  int wb = 0;
-  for (int a = 0; a < c.A; ++a)
-    for (int t = 0; t < c.T; ++t) {
-      step_set<PPT>(c, B, S, R, gi, so + a * c.T + t, a, t, wb, stat);
-      wb ^= 1;
-    }
-  __syncthreads();
-  const long long tc2 = clock64();
-
-  if (threadIdx.x == 0) {
-    S.rec[c.o_stats + 7] += stat[0];
-    S.rec[c.o_stats + 8] += stat[1];
-    S.rec[c.o_stats + 9] += stat[2];
-    S.bc[9] = env_epilogue(c, B, S, e) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  const bool done = S.bc[9] != 0.0;
-  write_tokens(c, B, S.rec, e, B.obs, true, !done);
-  long long tc3 = clock64(), tc4 = tc3;
-  if (done) {
-    write_tokens(c, B, S.rec, e, B.final_obs, false, false);
-    __syncthreads();
-    if (!spawn_env<PPT>(c, B, S, R, e, gi)) {
-      if (threadIdx.x == 0) atomicMax(status, (int)ST_SPAWN_INFEASIBLE);
+  uint32_t tphase = 0;
+  if (FULL && threadIdx.x == 0 && lo < hi) prefetch_set(B, S, set_off(B, lo), B.P);
+  long long cyc[kPhaseCount] = {0, 0, 0, 0};
+  for (int64_t e0 = lo; e0 < hi; e0 += blockDim.x) {
+    const int64_t e1 = min(hi, e0 + (int64_t)blockDim.x);
+    long long t0 = clock64();
+    // ---- 1. prologue, one env per thread
+    {
+      const int64_t e = e0 + threadIdx.x;
+      if (e < e1) env_prologue(cfg_of(Bg, e), Bg, e, B.env_index_offset + e, mode);
     }
     __syncthreads();
-    write_tokens(c, B, S.rec, e, B.obs, true, true);
-    tc4 = clock64();
+    long long t1 = clock64();
+    cyc[PH_PROLOGUE] += t1 - t0;
+    // ---- 2. every particle set of the chunk
+    for (int64_t e = e0; e < e1; ++e) {
+      const Rec rec = rec_of(B, e);
+      stage_env(cfg_of(B, e), B, S, rec, e);
+      __syncthreads();
+      const DevConfig& c = *S.cfg;
+      const int64_t gi = B.env_index_offset + e;
+      const int64_t so = set_off(B, e);
+      for (int a = 0; a < c.A; ++a)
+        for (int t = 0; t < c.T; ++t) {
+          const int64_t g = so + a * c.T + t;
+          step_set<PPT, FULL>(c, B, S, R, rec, gi, g, a, t, tphase, g + 1 < set_end ? g + 1 : -1);
+        }
+      __syncthreads();  // S.cfg / meas / mlist reused by the next env
+    }
+    long long t2 = clock64();
+    cyc[PH_FILTER] += t2 - t1;
+    // ---- 3. reward / done / info, one env per thread; then tokens
+    {
+      const int64_t e = e0 + threadIdx.x;
+      if (e < e1) S.flags[threadIdx.x] = env_epilogue(cfg_of(Bg, e), Bg, e) ? kChunkFlagDone : 0;
+    }
+    __syncthreads();
+    write_outputs(Bg, e0, e1, S.flags, 0, false);
+    write_outputs(Bg, e0, e1, S.flags, kChunkFlagDone, true);  // terminal obs of finished envs
+    long long t3 = clock64();
+    cyc[PH_OUTPUT] += t3 - t2;
+    // ---- 4. auto-reset of finished envs (vecenv.cpp:106-112)
+    bool any = false;
+    for (int i = 0; i < (int)(e1 - e0); ++i) any |= (S.flags[i] & kChunkFlagDone) != 0;
+    if (any) {
+      __syncthreads();
+      const int64_t e = e0 + threadIdx.x;
+      if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagDone)) {
+        if (spawn_serial(cfg_of(Bg, e), Bg, e, B.env_index_offset + e))
+          S.flags[threadIdx.x] |= kChunkFlagSpawned;
+        else
+          atomicMax(status, (int)ST_SPAWN_INFEASIBLE);
+      }
+      __syncthreads();
+      reinit_chunk<PPT>(Bg, e0, e1);
+      write_outputs(Bg, e0, e1, S.flags, kChunkFlagSpawned, false);
+      if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagSpawned)) B.step[e] = 0;
+    }
+    __syncthreads();
+    cyc[PH_RESET] += clock64() - t3;
   }
-  if (threadIdx.x == 0) B.step[e] = (int32_t)S.rec[R_STEP];
-  __syncthreads();
-  copy_rec(grec, S.rec, c.rec_words);
-  if (B.phase_cycles && threadIdx.x == 0) {
-    unsigned long long* pc = B.phase_cycles + e * kPhaseCount;
-    pc[PH_PROLOGUE] += (unsigned long long)(tc1 - tc0);
-    pc[PH_FILTER] += (unsigned long long)(tc2 - tc1);
-    pc[PH_OUTPUT] += (unsigned long long)(tc3 - tc2);
-    pc[PH_RESET] += (unsigned long long)(tc4 - tc3);
-  }
+  if (B.phase_cycles && threadIdx.x == 0)
+    for (int k = 0; k < kPhaseCount; ++k) B.phase_cycles[blockIdx.x * kPhaseCount + k] += (unsigned long long)cyc[k];
 }
 
 // Environment ctor / reset (env.cpp:110-151, 153-233) for every env. When
 // `ctor` is set the record starts zeroed and each set's stream is advanced past
 // pf::init's 8P draws (tracking.cpp:43-67), whose values spawn overwrites.
 template <int PPT>
-__global__ void reset_kernel(DevBatch B, int ctor, int32_t* status) {
+__global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) reset_kernel(DevBatch B, int ctor, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t e = blockIdx.x;
-  const DevConfig& c = cfg_of(B, e);
-  const Smem S = carve(smem_raw, c.rec_words, c.A, c.T, c.P);
-  BlockReducer R{S.red, 0};
-  const int64_t gi = B.env_index_offset + e;
-  double* grec = B.rec + rec_off(B, e);
-  if (ctor) {
-    for (int i = threadIdx.x; i < c.rec_words; i += blockDim.x) S.rec[i] = 0.0;
-    __syncthreads();
-    const int AT = c.A * c.T;
-    for (int i = threadIdx.x; i < AT; i += blockDim.x) {
-      S.rec[c.o_track + K_POS * AT + i] = 8.0 * (double)c.P;
-      S.rec[c.o_track + K_MAXSPEED * AT + i] = 1.0;
+  const Smem S = carve(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT, B.P);
+  const DevBatch& Bg = *B.self;
+  int64_t lo, hi;
+  cta_range(B.n_envs, lo, hi);
+  for (int64_t e0 = lo; e0 < hi; e0 += blockDim.x) {
+    const int64_t e1 = min(hi, e0 + (int64_t)blockDim.x);
+    const int64_t e = e0 + threadIdx.x;
+    if (e < e1) {
+      const DevConfig& c = cfg_of(B, e);
+      const Rec rec = rec_of(B, e);
+      if (ctor) {
+        for (int w = 0; w < c.rec_words; ++w) rec[w] = 0.0;
+        for (int a = 0; a < c.A; ++a)
+          for (int t = 0; t < c.T; ++t) {
+            TRK(K_POS, a * c.sT + t) = 8.0 * (double)c.P;
+            TRK(K_MAXSPEED, a * c.sT + t) = 1.0;
+          }
+        for (int a = 0; a < c.A; ++a) AG(V_RUDDER, a) = 2.0;
+        for (int t = 0; t < c.T; ++t) TG(V_RUDDER, t) = 2.0;
+      }
+      S.flags[threadIdx.x] = 0;
+      if (spawn_serial(cfg_of(Bg, e), Bg, e, B.env_index_offset + e))
+        S.flags[threadIdx.x] = kChunkFlagSpawned;
+      else
+        atomicMax(status, (int)ST_SPAWN_INFEASIBLE);
+      B.rewards[e] = 0.0;
+      B.dones[e] = 0;
+      B.step[e] = 0;
     }
-    for (int a = threadIdx.x; a < c.A; a += blockDim.x) S.rec[c.o_agent + V_RUDDER * c.A + a] = 2.0;
-    for (int t = threadIdx.x; t < c.T; t += blockDim.x) S.rec[c.o_target + V_RUDDER * c.T + t] = 2.0;
-  } else {
-    copy_rec(S.rec, grec, c.rec_words);
+    __syncthreads();
+    reinit_chunk<PPT>(Bg, e0, e1);
+    write_outputs(Bg, e0, e1, S.flags, 0, false);
+    __syncthreads();
   }
-  __syncthreads();
-  if (!spawn_env<PPT>(c, B, S, R, e, gi)) {
-    if (threadIdx.x == 0) atomicMax(status, (int)ST_SPAWN_INFEASIBLE);
-  }
-  __syncthreads();
-  write_tokens(c, B, S.rec, e, B.obs, true, true);
-  if (threadIdx.x == 0) {
-    B.rewards[e] = 0.0;
-    B.dones[e] = 0;
-    B.step[e] = (int32_t)S.rec[R_STEP];
-  }
-  __syncthreads();
-  copy_rec(grec, S.rec, c.rec_words);
 }
 
-// VecEnv::refresh_outputs (vecenv.cpp:145-150).
+// VecEnv::refresh_outputs (vecenv.cpp:145-150): one thread per row.
 __global__ void tokens_kernel(DevBatch B) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t e = blockIdx.x;
-  const DevConfig& c = cfg_of(B, e);
-  double* rec = reinterpret_cast<double*>(smem_raw);
-  copy_rec(rec, B.rec + rec_off(B, e), c.rec_words);
-  __syncthreads();
-  write_tokens(c, B, rec, e, B.obs, true, true);
-  if (threadIdx.x == 0) B.step[e] = (int32_t)rec[R_STEP];
+  const int Am = B.A_max, Rm = B.R_max;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < B.n_envs * Am * Rm; p += stride) {
+    const int64_t e = p / (Am * Rm);
+    const int q = (int)(p - e * Am * Rm), a = q / Rm, r = q - (q / Rm) * Rm;
+    double v[12];
+    token_row(cfg_of(B, e), rec_of(B, e), a, r, v);
+    const int64_t row = (e * Am + a) * Rm + r;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) B.obs[(int64_t)k * B.obs_rows + row] = v[k];
+  }
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < B.n_envs * Rm; p += stride) {
+    const int64_t e = p / Rm;
+    const int r = (int)(p - e * Rm);
+    double v[12];
+    global_row(cfg_of(B, e), rec_of(B, e), r, v);
+    const int64_t row = e * Rm + r;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) B.global[(int64_t)k * B.global_rows + row] = v[k];
+  }
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < B.n_envs * Am * 5; p += stride) {
+    const int64_t e = p / (Am * 5);
+    const int q = (int)(p - e * Am * 5), a = q / 5, k = q - (q / 5) * 5;
+    const DevConfig& c = cfg_of(B, e);
+    const Rec rec = rec_of(B, e);
+    B.masks[e * Am * 5 + q] = (a < c.A && abs(k - (int)AG(V_RUDDER, a)) <= 1) ? 1 : 0;
+  }
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B.n_envs; e += stride) {
+    const Rec rec = rec_of(B, e);
+    B.step[e] = (int32_t)rec[R_STEP];
+  }
 }
 
 // Action validation for VecEnv::step (env.cpp:236-248) before anything moves.
@@ -1206,10 +1329,10 @@ __global__ void validate_kernel(DevBatch B) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= B.n_envs) return;
   const DevConfig& c = cfg_of(B, e);
-  const double* rec = B.rec + rec_off(B, e);
+  const Rec rec = rec_of(B, e);
   for (int a = 0; a < c.A; ++a) {
     const int act = B.actions[e * B.A_max + a];
-    const int rud = (int)rec[c.o_agent + V_RUDDER * c.A + a];
+    const int rud = (int)AG(V_RUDDER, a);
     if (act < 0 || act >= 5 || abs(act - rud) > 1) {
       atomicMin(B.error_env, (int32_t)e);
       return;
@@ -1221,17 +1344,23 @@ __global__ void validate_kernel(DevBatch B) {
 __global__ void stats_kernel(DevBatch B, double* out, int reset) {
   __shared__ double red[kRedDoubles];
   BlockReducer R{red, 0};
+  const int o_stats = B.cfgs[0].o_stats;
   for (int k = 0; k < kStatCount; ++k) {
     double acc = 0.0;
+    double* st = B.rec + (int64_t)(o_stats + k) * B.n_envs;
     for (int64_t e = threadIdx.x; e < B.n_envs; e += blockDim.x) {
-      const DevConfig& c = cfg_of(B, e);
-      double* st = B.rec + rec_off(B, e) + c.o_stats;
-      acc = acc + st[k];
-      if (reset) st[k] = 0.0;
+      acc = acc + st[e];
+      if (reset) st[e] = 0.0;
     }
     const double s = R.sum(acc);
     if (threadIdx.x == 0) out[k] = s;
   }
 }
+
+#undef AG
+#undef TG
+#undef INFO
+#undef TRK
+#undef STAT
 
 }  // namespace ut

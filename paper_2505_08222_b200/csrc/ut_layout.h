@@ -4,12 +4,16 @@
 //  1. the particle store, structure-of-arrays: px/py/vx/vy/w each [set][P] fp64,
 //     set = set_offset[env] + agent * T + target -- one 8 KB contiguous chunk per
 //     set and field at P = 1024 (ParticleSet, tracking.hpp:39-55);
-//  2. one env record per env (rec_offset[env], `rec_words` fp64 words): every
-//     other piece of Environment state (env.hpp:44-51, 131-171) as small SoA
-//     arrays inside the record, staged whole through shared memory by the CTA
-//     that steps the env. Integer fields are stored as exact fp64 values, like
-//     the reference's own state blob (env.cpp:550-593);
-//  3. the batch output buffers of VecEnv (vecenv.hpp:51-62), column-major.
+//  2. every other piece of Environment state (env.hpp:44-51, 131-171) as one
+//     fp64 array per scalar field, structure-of-arrays ACROSS envs: word w of
+//     env e lives at rec[w * n_envs + e], so when thread i of a CTA runs the
+//     serial per-env phases of env (base + i) every field access is coalesced.
+//     Integer fields are stored as exact fp64 values, like the reference's own
+//     state blob (env.cpp:550-593). Field words are laid out for the batch's
+//     largest fleet (sA x sT) so mixed fleets share one index space;
+//  3. per-step scratch: the ping schedule the prologue hands to the particle
+//     phase (horizontal ranges, ping-present and comm-link flags);
+//  4. the batch output buffers of VecEnv (vecenv.hpp:51-62), column-major.
 #pragma once
 #include <stdint.h>
 
@@ -49,19 +53,25 @@ struct DevConfig {
   double min_sep, disc_r, pert_std, depth_min, depth_max;
   double pn, vn, speed_margin, init_radius;
   double head_a, head_b, head_noise, max_turn;
-  // record layout (fp64 word offsets)
+  // record layout (field-word offsets) for the batch strides sA >= A, sT >= T:
+  // agent field f of agent a: o_agent + f sA + a; target: o_target + f sT + t;
+  // AgentInfo f of (r, s): o_info + f sA^2 + r sA + s; track f of (a, t):
+  // o_track + f sA sT + a sT + t.
+  int sA, sT;
   int o_agent, o_target, o_miss, o_info, o_track, o_stats, rec_words, _pad;
 };
 
-__host__ __device__ inline void layout_config(DevConfig& c) {
+__host__ __device__ inline void layout_config(DevConfig& c, int sA, int sT) {
   c.R = c.A + c.T;
+  c.sA = sA;
+  c.sT = sT;
   c.o_agent = R_NSCALAR;
-  c.o_target = c.o_agent + 6 * c.A;
-  c.o_miss = c.o_target + 8 * c.T;
-  c.o_info = c.o_miss + c.T;
-  c.o_track = c.o_info + I_NFIELD * c.A * c.A;
-  c.o_stats = c.o_track + K_NFIELD * c.A * c.T;
-  c.rec_words = (c.o_stats + kStatCount + 1) & ~1;
+  c.o_target = c.o_agent + 6 * sA;
+  c.o_miss = c.o_target + 8 * sT;
+  c.o_info = c.o_miss + sT;
+  c.o_track = c.o_info + I_NFIELD * sA * sA;
+  c.o_stats = c.o_track + K_NFIELD * sA * sT;
+  c.rec_words = c.o_stats + kStatCount;
 }
 
 // Per-batch constant tables (device pointers) passed to every kernel.
@@ -73,9 +83,10 @@ struct DevBatch {
   int A_max, T_max, R_max, P;
   const DevConfig* cfgs;      // [n_cfg]
   const int32_t* cfg_of_env;  // [n_envs] or nullptr (homogeneous)
-  const int64_t* rec_offset;  // [n_envs] words, or nullptr: env * rec_words(cfg 0)
   const int64_t* set_offset;  // [n_envs] sets, or nullptr: env * A * T
-  double* rec;
+  double* rec;                // [rec_words][n_envs]
+  double* sched_r2;           // [n_envs][sA * sT] horizontal ranges this step
+  uint8_t* sched_flags;       // [n_envs][sA * sT + sA * sA] ping present | link
   double *px, *py, *vx, *vy, *w;
   // batch outputs
   int64_t obs_rows, global_rows;
@@ -97,9 +108,12 @@ struct DevBatch {
   // path; printf a per-set trace for one env (-1 = off)
   int32_t force_exact;
   int64_t trace_env;
-  // Phase timing (PhaseTimer, env.cpp:18-36): SM cycles per env accumulated in
-  // [n_envs][kPhaseCount] when non-null.
+  // Phase timing (PhaseTimer, env.cpp:18-36): SM cycles per CTA accumulated in
+  // [grid][kPhaseCount] when non-null.
   unsigned long long* phase_cycles;
+  // Device copy of this struct, for the out-of-line (cold) device functions, so
+  // the kernel's by-value parameter is never address-taken.
+  const struct DevBatch* self;
 };
 
 // Device phases (the reference's seven StepPhase values, env.hpp:71-80, map onto

@@ -251,9 +251,11 @@ def test_cr_math_exhaustive_on_device(cuda_device):
     got = np.empty(1 << 24, np.float32)
     for kind in range(3):
         o.uto_cr_grid(kind, want.ctypes.data)
-        assert lib.ut_debug_cr_grid(kind, 0, got.ctypes.data) == 0
-        bad = np.flatnonzero(got.view(np.uint32) != want.view(np.uint32))
-        assert bad.size == 0, (kind, bad[:10])
+        # kind: fp64-libm reference path; kind + 3: the table-driven production path
+        for dev_kind in (kind, kind + 3):
+            assert lib.ut_debug_cr_grid(dev_kind, 0, got.ctypes.data) == 0
+            bad = np.flatnonzero(got.view(np.uint32) != want.view(np.uint32))
+            assert bad.size == 0, (dev_kind, bad[:10])
 
 
 def test_philox_and_keys_on_device(cuda_device):
