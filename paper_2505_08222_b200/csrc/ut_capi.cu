@@ -203,17 +203,25 @@ struct ut_vecenv {
     return UT_OK;
   }
 
+  int np = 1024;              // particle capacity of the step kernel instance
+  size_t smem_reset = 0;      // the reset kernel always uses the 1024 layout
+
   int launch_step(int mode) {
-    if (full)
-      step_kernel<kPPT, true><<<(unsigned)grid, nt, smem, stream>>>(B, mode, d_status);
+    const dim3 g((unsigned)grid), b((unsigned)nt);
+    if (full && np == 1024)
+      step_kernel<kPPT, 1024, true><<<g, b, smem, stream>>>(B, mode, d_status);
+    else if (full && np == 512)
+      step_kernel<kPPT, 512, true><<<g, b, smem, stream>>>(B, mode, d_status);
+    else if (full && np == 256)
+      step_kernel<kPPT, 256, true><<<g, b, smem, stream>>>(B, mode, d_status);
     else
-      step_kernel<kPPT, false><<<(unsigned)grid, nt, smem, stream>>>(B, mode, d_status);
+      step_kernel<kPPT, 1024, false><<<g, b, smem, stream>>>(B, mode, d_status);
     ++launches;
     UT_CUDA(cudaGetLastError());
     return UT_OK;
   }
   int launch_reset(int ctor) {
-    reset_kernel<kPPT><<<(unsigned)grid, nt, smem, stream>>>(B, ctor, d_status);
+    reset_kernel<kPPT, 1024><<<(unsigned)grid, nt, smem_reset, stream>>>(B, ctor, d_status);
     ++launches;
     UT_CUDA(cudaGetLastError());
     return UT_OK;
@@ -330,22 +338,35 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   UT_CUDA(cudaMemsetAsync(B.sched_flags, 0, n_envs * (Am * Tm + Am * Am), v->stream));
 
   v->nt = threads_for(v->P);
-  v->smem = smem_bytes(v->A_max, v->T_max, v->P, v->nt);
   int max_optin = 0, sms = 0;
   UT_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  if ((int)v->smem > max_optin)
-    return fail(UT_ERR_CONFIG, "configuration needs %zu B of shared memory per CTA (max %d)", v->smem, max_optin);
-  v->full = (v->P == v->nt * kPPT) && (v->P % 4 == 0);
-  UT_CUDA(cudaFuncSetAttribute(step_kernel<kPPT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
-  UT_CUDA(cudaFuncSetAttribute(step_kernel<kPPT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
-  UT_CUDA(cudaFuncSetAttribute(reset_kernel<kPPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
+  // FULL instances: P == nt * PPT with a compile-time particle capacity
+  v->full = (v->P == v->nt * kPPT) && (v->P == 1024 || v->P == 512 || v->P == 256);
+  v->np = v->full ? v->P : 1024;
+  const void* fn = nullptr;
+  if (v->np == 1024 && v->full) {
+    fn = (const void*)step_kernel<kPPT, 1024, true>;
+    v->smem = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
+  } else if (v->np == 512) {
+    fn = (const void*)step_kernel<kPPT, 512, true>;
+    v->smem = smem_bytes<512>(v->A_max, v->T_max, v->nt);
+  } else if (v->np == 256) {
+    fn = (const void*)step_kernel<kPPT, 256, true>;
+    v->smem = smem_bytes<256>(v->A_max, v->T_max, v->nt);
+  } else {
+    fn = (const void*)step_kernel<kPPT, 1024, false>;
+    v->smem = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
+  }
+  v->smem_reset = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
+  if ((int)v->smem_reset > max_optin)
+    return fail(UT_ERR_CONFIG, "configuration needs %zu B of shared memory per CTA (max %d)", v->smem_reset, max_optin);
+  UT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
+  UT_CUDA(cudaFuncSetAttribute((const void*)reset_kernel<kPPT, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)v->smem_reset));
   // persistent grid: every resident CTA slot, each owning a contiguous env range
   int per_sm = 0;
-  if (v->full)
-    UT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<kPPT, true>, v->nt, v->smem));
-  else
-    UT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<kPPT, false>, v->nt, v->smem));
+  UT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v->nt, v->smem));
   if (per_sm < 1) return fail(UT_ERR_RUNTIME, "step kernel cannot be resident with %zu B shared memory", v->smem);
   v->grid = (int)std::min<int64_t>(n_envs, (int64_t)per_sm * sms);
   if ((rc = v->alloc(&v->d_self, 1))) return rc;

@@ -74,40 +74,49 @@ __host__ __device__ inline size_t resample_bytes(int P) {
   return align16(a > b ? a : b);
 }
 
-__host__ __device__ inline size_t smem_bytes(int sA, int sT, int P, int nt) {
-  size_t s = 0;
-  s += sizeof(double2) * (128 + 64) + sizeof(double) * 32;
-  s += align16(sizeof(DevConfig));
-  s += align16(sizeof(double) * kRedDoubles);
-  s += align16(sizeof(double) * 16);
-  s += sizeof(uint4) * 32 * 5;
+// Fixed-size part of the layout for a particle capacity NP (compile-time
+// offsets: every access is an LDS/STS with an immediate offset). The
+// fleet-sized regions follow at runtime offsets.
+template <int NP>
+struct FixedSmem {
+  double2 tab_log[128];
+  double2 tab_sc[64];
+  double tab_exp[32];
+  double red[kRedDoubles];
+  double bc[16];
+  uint4 xch[32 * 5];
+  uint64_t mbar[2];
+  double pf[5 * NP];
+  double area[(5 * NP > 4 * NP + 4 ? 5 * NP : 4 * NP + 4)];  // resample cum + staging | re-init words
+  DevConfig cfg;
+};
+
+template <int NP>
+__host__ __device__ inline size_t smem_bytes(int sA, int sT, int nt) {
+  size_t s = align16(sizeof(FixedSmem<NP>));
   s += align16(sizeof(double) * kMeasStride * sA * sT);
   s += align16(sizeof(uint16_t) * sA * sT);
   s += align16(sizeof(uint16_t) * sA * sT * sA);
   s += align16(nt);
-  s += 16;
-  s += align16(sizeof(double) * 5 * (size_t)P);
-  s += resample_bytes(P);
   return s;
 }
 
-__device__ inline Smem carve(unsigned char* base, int sA, int sT, int P) {
+template <int NP>
+__device__ __forceinline__ Smem carve(unsigned char* base, int sA, int sT) {
+  FixedSmem<NP>& F = *reinterpret_cast<FixedSmem<NP>*>(base);
   Smem S;
-  size_t o = 0;
-  S.tab_log = (double2*)(base + o);
-  o += sizeof(double2) * 128;
-  S.tab_sc = (double2*)(base + o);
-  o += sizeof(double2) * 64;
-  S.tab_exp = (double*)(base + o);
-  o += sizeof(double) * 32;
-  S.cfg = (DevConfig*)(base + o);
-  o += align16(sizeof(DevConfig));
-  S.red = (double*)(base + o);
-  o += align16(sizeof(double) * kRedDoubles);
-  S.bc = (double*)(base + o);
-  o += align16(sizeof(double) * 16);
-  S.xch = (uint4*)(base + o);
-  o += sizeof(uint4) * 32 * 5;
+  S.tab_log = F.tab_log;
+  S.tab_sc = F.tab_sc;
+  S.tab_exp = F.tab_exp;
+  S.cfg = &F.cfg;
+  S.red = F.red;
+  S.bc = F.bc;
+  S.xch = F.xch;
+  S.mbar = F.mbar;
+  S.pf = F.pf;
+  S.cum = F.area;
+  S.st = F.area + NP;
+  size_t o = align16(sizeof(FixedSmem<NP>));
   S.meas = (double*)(base + o);
   o += align16(sizeof(double) * kMeasStride * sA * sT);
   S.mcount = (uint16_t*)(base + o);
@@ -115,19 +124,13 @@ __device__ inline Smem carve(unsigned char* base, int sA, int sT, int P) {
   S.mlist = (uint16_t*)(base + o);
   o += align16(sizeof(uint16_t) * sA * sT * sA);
   S.flags = base + o;
-  o += align16(blockDim.x);
-  S.mbar = (uint64_t*)(base + o);
-  o += 16;
-  S.pf = (double*)(base + o);
-  o += align16(sizeof(double) * 5 * (size_t)P);
-  S.cum = (double*)(base + o);
-  S.st = S.cum + P;
   return S;
 }
 
-__device__ __forceinline__ Smem carve_dyn(int sA, int sT, int P) {
+template <int NP>
+__device__ __forceinline__ Smem carve_dyn(int sA, int sT) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  return carve(smem_raw, sA, sT, P);
+  return carve<NP>(smem_raw, sA, sT);
 }
 
 __device__ __forceinline__ const DevConfig& cfg_of(const DevBatch& B, int64_t e) {
@@ -897,16 +900,18 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     // way; all others have products >= 2^-60 max(e) >= 2^-920 (normal) when
     // max(e) >= 2^-860, and no stage can degenerate. So under that check the
     // merged result equals the sequential one to rounding; otherwise (or with a
-    // non-finite shift) the exact sequential path runs.
+    // non-finite shift) the exact sequential path runs. The argument holds for
+    // any UPPER BOUND s'_j >= s_j (e only shrinks, the guard stays
+    // conservative), so the stage maxima are taken in fp32 rounded up.
     double L[PPT];
 #pragma unroll
     for (int q = 0; q < PPT; ++q) L[q] = 0.0;
-    double* mb = R.buf();  // per-stage warp maxima, [stage * 32 + warp]
+    float* mb = reinterpret_cast<float*>(R.buf());  // per-stage warp maxima, [stage * 32 + warp]
 #pragma unroll 1
     for (int j = 0; j < nm; ++j) {
       const double* m = S.meas + kMeasStride * ml[j];
       const double ox = m[0], oy = m[1], r2 = m[2], sig = m[3], rsig = m[4];
-      double mj = -CUDART_INF;
+      float mj = -CUDART_INF_F;
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         if (FULL || k0 + q < P) {
@@ -915,31 +920,26 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           const double qv = div_rcp(d - r2, sig, rsig);
           const double ll = 0.0 - 0.5 * (qv * qv);
           L[q] = L[q] + ll;
-          mj = ll > mj ? ll : mj;
+          mj = fmaxf(mj, __double2float_ru(ll));
         }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double u = __shfl_xor_sync(0xffffffffu, mj, o);
-        mj = u > mj ? u : mj;
-      }
+      for (int o = 16; o > 0; o >>= 1) mj = fmaxf(mj, __shfl_xor_sync(0xffffffffu, mj, o));
       if (lane == 0) mb[j * 32 + warp] = mj;
     }
     __syncthreads();
-    double shift = 0.0;  // sum_j s_j, in stage order
+    double shift = 0.0;  // sum_j s'_j, in stage order
 #pragma unroll 1
     for (int j = 0; j < nm; ++j) {
-      double sj = -CUDART_INF;
-      for (int v = 0; v < nw; ++v) {
-        const double u = mb[j * 32 + v];
-        sj = u > sj ? u : sj;
-      }
-      shift = j == 0 ? sj : shift + sj;
+      float sj = mb[j * 32];
+      for (int v = 1; v < nw; ++v) sj = fmaxf(sj, mb[j * 32 + v]);
+      shift = j == 0 ? (double)sj : shift + (double)sj;
     }
     if (!isfinite(shift)) {
       exact = true;
     } else {
-      double e[PPT], ls = 0.0, lq = 0.0, lm = 0.0;
+      double e[PPT], ls = 0.0, lq = 0.0;
+      int lx = 0;  // max biased exponent of e
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         e[q] = 0.0;
@@ -947,16 +947,16 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           e[q] = s.w[q] * exp_neg(L[q] - shift, S.tab_exp);
           ls = ls + e[q];
           lq = lq + e[q] * e[q];
-          lm = e[q] > lm ? e[q] : lm;
+          lx = max(lx, __double2hiint(e[q]) >> 20);
         }
       }
-      const double3 r = R.sum2_max(ls, lq, lm);
-      if (isfinite(r.x) && r.x > 0.0 && r.z >= kMergeFloor) {
+      const double2 r = R.sum2_imax(ls, lq, lx);
+      if (isfinite(r.x) && r.x > 0.0 && lx >= 1023 - 860) {  // max(e) >= 2^-860
         const double rcp = 1.0 / r.x;
 #pragma unroll
         for (int q = 0; q < PPT; ++q) s.w[q] = div_rcp(e[q], r.x, rcp);
         // ESS = sum^2 / sum(e^2) unless the squares may have underflowed
-        if (r.z >= 0x1p-200) {
+        if (lx >= 1023 - 200) {
           ess = (r.x * r.x) / r.y;
           have_ess = true;
         }
@@ -1146,9 +1146,9 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
 
 // Re-init every set of the chunk's envs flagged kChunkFlagSpawned (out of line:
 // works on the global copy of the batch descriptor and the dynamic smem).
-template <int PPT>
+template <int PPT, int NP>
 __device__ __noinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t e1) {
-  const Smem S = carve_dyn(B.cfgs[0].sA, B.cfgs[0].sT, B.P);
+  const Smem S = carve_dyn<NP>(B.cfgs[0].sA, B.cfgs[0].sT);
   BlockReducer R{S.red, 0};
   for (int64_t e = e0; e < e1; ++e) {
     if (!(S.flags[e - e0] & kChunkFlagSpawned)) continue;
@@ -1170,10 +1170,10 @@ __device__ __noinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t
 #endif
 
 // The fused step.
-template <int PPT, bool FULL>
+template <int PPT, int NP, bool FULL>
 __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem S = carve(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT, B.P);
+  const Smem S = carve<NP>(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT);
   const DevBatch& Bg = *B.self;  // cold paths read the global copy
   BlockReducer R{S.red, 0};
   load_tables(S);
@@ -1236,7 +1236,7 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
           atomicMax(status, (int)ST_SPAWN_INFEASIBLE);
       }
       __syncthreads();
-      reinit_chunk<PPT>(Bg, e0, e1);
+      reinit_chunk<PPT, NP>(Bg, e0, e1);
       write_outputs(Bg, e0, e1, S.flags, kChunkFlagSpawned, false);
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagSpawned)) B.step[e] = 0;
     }
@@ -1250,10 +1250,10 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
 // Environment ctor / reset (env.cpp:110-151, 153-233) for every env. When
 // `ctor` is set the record starts zeroed and each set's stream is advanced past
 // pf::init's 8P draws (tracking.cpp:43-67), whose values spawn overwrites.
-template <int PPT>
+template <int PPT, int NP>
 __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) reset_kernel(DevBatch B, int ctor, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem S = carve(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT, B.P);
+  const Smem S = carve<NP>(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT);
   const DevBatch& Bg = *B.self;
   int64_t lo, hi;
   cta_range(B.n_envs, lo, hi);
@@ -1283,7 +1283,7 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) reset_kernel(DevBatch
       B.step[e] = 0;
     }
     __syncthreads();
-    reinit_chunk<PPT>(Bg, e0, e1);
+    reinit_chunk<PPT, NP>(Bg, e0, e1);
     write_outputs(Bg, e0, e1, S.flags, 0, false);
     __syncthreads();
   }
