@@ -770,23 +770,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   const bool noise = c.noise_on != 0;
   const uint64_t u0p = pos + (noise ? 4ull * (uint64_t)P : 0ull);  // resample draw follows predict
 
-  // ---- particles into registers
+  // ---- particles into registers (FULL: after the noise is drawn, below, so the
+  // Box-Muller pairs of all PPT particles can be interleaved)
   SetRegs<PPT> s;
-  if (FULL) {
-    mbar_wait(S.mbar, tphase);
-    tphase ^= 1u;
-#pragma unroll
-    for (int q = 0; q < PPT; q += 2) {
-      const double2 x = *reinterpret_cast<const double2*>(S.pf + k0 + q);
-      const double2 y = *reinterpret_cast<const double2*>(S.pf + P + k0 + q);
-      const double2 u = *reinterpret_cast<const double2*>(S.pf + 2 * P + k0 + q);
-      const double2 v = *reinterpret_cast<const double2*>(S.pf + 3 * P + k0 + q);
-      const double2 w = *reinterpret_cast<const double2*>(S.pf + 4 * P + k0 + q);
-      s.px[q] = x.x, s.px[q + 1] = x.y, s.py[q] = y.x, s.py[q + 1] = y.y;
-      s.vx[q] = u.x, s.vx[q + 1] = u.y, s.vy[q] = v.x, s.vy[q + 1] = v.y;
-      s.w[q] = w.x, s.w[q + 1] = w.y;
-    }
-  } else {
+  if (!FULL) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       const int k = k0 + j;
@@ -826,17 +813,12 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     reinterpret_cast<uint32_t*>(S.bc)[0] = w2[0];
     reinterpret_cast<uint32_t*>(S.bc)[1] = w2[1];
   }
-  __syncthreads();  // set-start barrier: S.pf consumed, xch / u0 published
-  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
+  __syncthreads();  // set-start barrier: xch / u0 published
   const uint64_t u0_lo = reinterpret_cast<const uint32_t*>(S.bc)[0];
   const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
 
-  // ---- pf::predict (tracking.cpp:94-117)
-#pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    s.px[j] = s.px[j] + s.vx[j] * c.dt;
-    s.py[j] = s.py[j] + s.vy[j] * c.dt;
-  }
+  // ---- pf::predict (tracking.cpp:94-117): the normals first
+  float zpx[PPT], zpy[PPT], zvx[PPT], zvy[PPT];  // out[k], out[P+k], out[2P+k], out[3P+k]
   if (noise) {
     uint32_t W[4][4];  // [segment][particle]
     if (FULL) {
@@ -856,24 +838,51 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         for (int q = 0; q < 4; ++q)
           W[q][j] = k0 + j < P ? word_at(key, (uint64_t)ps, pos + (uint64_t)q * (uint64_t)P + (uint64_t)(k0 + j)) : 0u;
     }
+    // pair k: u1 = word(pos+k), u2 = word(pos+2P+k); pair P+k: segments 1, 3
+    bool ok = true;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      if (FULL || k0 + j < P) {
-        // pair k: u1 = word(pos+k), u2 = word(pos+2P+k); pair P+k: segments 1, 3
-        float zpx, zvx, zpy, zvy;  // out[k], out[2P+k] / out[P+k], out[3P+k]
-        bool ok = box_muller_fast(W[0][j], W[2][j], S.tab_log, S.tab_sc, zpx, zvx);
-        ok &= box_muller_fast(W[1][j], W[3][j], S.tab_log, S.tab_sc, zpy, zvy);
-        if (!ok) {  // an uncertain rounding (p ~ 1e-4 per particle): exact fp64 libm path
-          box_muller_slow(W[0][j], W[2][j], zpx, zvx);
-          box_muller_slow(W[1][j], W[3][j], zpy, zvy);
-        }
-        s.px[j] = s.px[j] + c.pn * (double)zpx;
-        s.py[j] = s.py[j] + c.pn * (double)zpy;
-        s.vx[j] = s.vx[j] + c.vn * (double)zvx;
-        s.vy[j] = s.vy[j] + c.vn * (double)zvy;
+      ok &= box_muller_fast(W[0][j], W[2][j], S.tab_log, S.tab_sc, zpx[j], zvx[j]);
+      ok &= box_muller_fast(W[1][j], W[3][j], S.tab_log, S.tab_sc, zpy[j], zvy[j]);
+    }
+    if (!ok) {  // an uncertain rounding (p ~ 1e-4 per particle): exact fp64 libm path
+#pragma unroll 1
+      for (int j = 0; j < PPT; ++j) {
+        box_muller_slow(W[0][j], W[2][j], zpx[j], zvx[j]);
+        box_muller_slow(W[1][j], W[3][j], zpy[j], zvy[j]);
       }
     }
     pos += 4ull * (uint64_t)P;
+  }
+  if (FULL) {
+    mbar_wait(S.mbar, tphase);
+    tphase ^= 1u;
+#pragma unroll
+    for (int q = 0; q < PPT; q += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(S.pf + k0 + q);
+      const double2 y = *reinterpret_cast<const double2*>(S.pf + P + k0 + q);
+      const double2 u = *reinterpret_cast<const double2*>(S.pf + 2 * P + k0 + q);
+      const double2 v = *reinterpret_cast<const double2*>(S.pf + 3 * P + k0 + q);
+      const double2 w = *reinterpret_cast<const double2*>(S.pf + 4 * P + k0 + q);
+      s.px[q] = x.x, s.px[q + 1] = x.y, s.py[q] = y.x, s.py[q + 1] = y.y;
+      s.vx[q] = u.x, s.vx[q + 1] = u.y, s.vy[q] = v.x, s.vy[q + 1] = v.y;
+      s.w[q] = w.x, s.w[q + 1] = w.y;
+    }
+    __syncthreads();  // S.pf consumed
+    if (tid == 0 && next >= 0) prefetch_set(B, S, next, P);
+  }
+#pragma unroll
+  for (int j = 0; j < PPT; ++j) {
+    if (FULL || k0 + j < P) {
+      s.px[j] = s.px[j] + s.vx[j] * c.dt;
+      s.py[j] = s.py[j] + s.vy[j] * c.dt;
+      if (noise) {
+        s.px[j] = s.px[j] + c.pn * (double)zpx[j];
+        s.py[j] = s.py[j] + c.pn * (double)zpy[j];
+        s.vx[j] = s.vx[j] + c.vn * (double)zvx[j];
+        s.vy[j] = s.vy[j] + c.vn * (double)zvy[j];
+      }
+    }
   }
   if (ms > 0.0) {
 #pragma unroll
@@ -916,7 +925,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       for (int q = 0; q < PPT; ++q) {
         if (FULL || k0 + q < P) {
           const double dx = s.px[q] - ox, dy = s.py[q] - oy;
-          const double d = sqrt(dx * dx + dy * dy);
+          const double d = sqrt_dist(dx * dx + dy * dy);
           const double qv = div_rcp(d - r2, sig, rsig);
           const double ll = 0.0 - 0.5 * (qv * qv);
           L[q] = L[q] + ll;
