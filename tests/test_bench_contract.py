@@ -1,0 +1,40 @@
+"""CPU: bench.py's contract pieces that do not need a GPU -- the algorithmic
+byte count behind the roofline and the reference arm, which times
+the reference's own CPU step (oracle/_ref) on this host."""
+import json
+import subprocess
+import sys
+
+import pytest
+
+from oracle_bindings import ROOT, ref_available
+
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+
+
+def test_algorithmic_bytes_match_survey():
+    """0.083 MB (C1), 0.330 MB (C2), 2.059 MB (C3) per env-step."""
+    for name, A, T, want in (("c1", 1, 1, 0.083e6), ("c2", 2, 2, 0.330e6), ("c3", 5, 5, 2.059e6)):
+        got = bench.algorithmic_bytes_per_env_step(A, T, 1024, bench.rec_words_for(A, T))
+        assert abs(got - want) / want < 0.02, (name, got)
+
+
+def test_particle_bytes_dominate():
+    A = T = 5
+    total = bench.algorithmic_bytes_per_env_step(A, T, 1024, bench.rec_words_for(A, T))
+    assert 80 * 1024 * A * T / total > 0.95
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built")
+def test_reference_arm_prints_one_json_line():
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--config", "c1",
+                        "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["unit"] == "agent-env steps/s"
