@@ -48,6 +48,9 @@ __device__ __forceinline__ Rec rec_of(const DevBatch& B, int64_t e) { return Rec
 #define STAT(k) rec[c.o_stats + (k)]
 
 // ------------------------------------------------------------ smem carve ---
+// staged per-set scalars (Smem::trk)
+enum : int { TK_POS = 0, TK_MAXSPEED, TK_EX, TK_EY, TK_ESSOK, TK_AGE, TK_EVER, TK_KEY, kTrkStride };
+
 struct Smem {
   double2* tab_log;  // [128]
   double2* tab_sc;   // [64]
@@ -59,6 +62,7 @@ struct Smem {
   double* meas;      // [sA*sT][kMeasStride] pings of the env being filtered
   uint16_t* mcount;  // [sA*sT] measurements applied to each set this step
   uint16_t* mlist;   // [sA*sT][sA] their meas indices in application order
+  double* trk;       // [sA*sT][kTrkStride] the sets' track scalars + PF stream keys
   uint8_t* flags;    // [blockDim] per-env chunk flags
   uint64_t* mbar;    // TMA completion barrier
   double* pf;        // [5][P] TMA-prefetched next particle set
@@ -97,6 +101,7 @@ __host__ __device__ inline size_t smem_bytes(int sA, int sT, int nt) {
   s += align16(sizeof(double) * kMeasStride * sA * sT);
   s += align16(sizeof(uint16_t) * sA * sT);
   s += align16(sizeof(uint16_t) * sA * sT * sA);
+  s += align16(sizeof(double) * kTrkStride * sA * sT);
   s += align16(nt);
   return s;
 }
@@ -123,6 +128,8 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int sA, int sT) {
   o += align16(sizeof(uint16_t) * sA * sT);
   S.mlist = (uint16_t*)(base + o);
   o += align16(sizeof(uint16_t) * sA * sT * sA);
+  S.trk = (double*)(base + o);
+  o += align16(sizeof(double) * kTrkStride * sA * sT);
   S.flags = base + o;
   return S;
 }
@@ -657,9 +664,9 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
 template <int PPT, bool FULL>
 __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Smem& S) {
   const int tid = threadIdx.x;
-  double* cum = S.cum;
+  int* mark = reinterpret_cast<int*>(S.cum);  // [P] first output of each particle
   double* st = S.st;
-  double* wsum = S.red + 2 * kRedSlots;
+  double* wsum = S.red + 2 * kRedSlots;  // [32] warp totals, [32] lane-31 excl, [32] lane-31 run, [32] int maxima
   double loc[PPT];
   double run = 0.0;
 #pragma unroll
@@ -683,57 +690,81 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   }
   double excl = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) excl = 0.0;
-  if (lane == 31) wsum[warp] = incl;
-  __syncthreads();
-  double woff = 0.0;
-  for (int v = 0; v < warp; ++v) woff = woff + wsum[v];
-  const double base = woff + excl;
+  if (lane == 31) {
+    wsum[warp] = incl;
+    wsum[32 + warp] = excl;
+    wsum[64 + warp] = run;
+  }
 #pragma unroll
   for (int q = 0; q < PPT; ++q)
-    if (FULL || k0 + q < P) cum[k0 + q] = base + loc[q];
+    if (FULL || k0 + q < P) mark[k0 + q] = -1;
   __syncthreads();
-  const double inv_n = 1.0 / (double)P;
-  if (FULL || k0 < P) {
-    const double u = ((double)k0 + u0) * inv_n;
-    int a = 0, b = P - 1;
-    while (a < b) {
-      const int mid = (a + b) >> 1;
-      if (cum[mid] < u)
-        a = mid + 1;
-      else
-        b = mid;
-    }
-    int i = a;
+  // cum[k] = base + loc[q] (the scan's values); cum[k0 - 1] exactly as the
+  // previous thread computes it
+  double woff = 0.0, woff_prev = 0.0;
+  for (int v = 0; v < warp; ++v) {
+    woff_prev = woff;
+    woff = woff + wsum[v];
+  }
+  const double base = woff + excl;
+  double c[PPT];
 #pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-      const int j = k0 + q;
-      if (FULL || j < P) {
-        const double uj = ((double)j + u0) * inv_n;
-        // lower_bound over [i, P-1]: usually i or i+1; otherwise a binary search
-        // (a plain forward walk diverges over runs of zero-weight particles)
-        if (i < P - 1 && cum[i] < uj) {
-          ++i;
-          if (i < P - 1 && cum[i] < uj) {
-            int lo = i + 1, hi = P - 1;
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              if (cum[mid] < uj)
-                lo = mid + 1;
-              else
-                hi = mid;
-            }
-            i = lo;
-          }
-        }
-        s.px[q] = st[i];
-        s.py[q] = st[P + i];
-        s.vx[q] = st[2 * P + i];
-        s.vy[q] = st[3 * P + i];
-        s.w[q] = inv_n;
-      }
+  for (int q = 0; q < PPT; ++q) c[q] = base + loc[q];
+  double cprev = __shfl_up_sync(0xffffffffu, c[PPT - 1], 1);
+  if (lane == 0 && warp > 0) cprev = (woff_prev + wsum[32 + warp - 1]) + wsum[64 + warp - 1];
+  // Output j takes the first particle i with cum[i] >= u_j, u_j = (j + u0)/n
+  // (clamped to n - 1): particle i owns outputs [count(cum[i-1]), count(cum[i]))
+  // with count(c) = #{j : u_j <= c}; it marks the first one and a prefix max
+  // over the marks hands every output its source.
+  const double inv_n = 1.0 / (double)P;
+  auto count_le = [&](double cv) -> int {
+    const double x = cv * (double)P - u0;
+    int m = x < 0.0 ? 0 : (x >= (double)P ? P : (int)x + 1);
+    while (m > 0 && ((double)(m - 1) + u0) * inv_n > cv) --m;
+    while (m < P && ((double)m + u0) * inv_n <= cv) ++m;
+    return m;
+  };
+  int lo = tid == 0 ? 0 : count_le(cprev);
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    const int k = k0 + q;
+    if (FULL || k < P) {
+      const int hi = k == P - 1 ? P : count_le(c[q]);
+      if (hi > lo) mark[lo] = k;
+      lo = hi;
     }
   }
   __syncthreads();
+  int r[PPT];
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    r[q] = (FULL || k0 + q < P) ? mark[k0 + q] : -1;
+    if (q > 0) r[q] = max(r[q], r[q - 1]);
+  }
+  int mi = r[PPT - 1];
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, mi, o);
+    if (lane >= o) mi = max(mi, y);
+  }
+  int mex = __shfl_up_sync(0xffffffffu, mi, 1);
+  if (lane == 0) mex = -1;
+  int* wmx = reinterpret_cast<int*>(wsum + 96);
+  if (lane == 31) wmx[warp] = mi;
+  __syncthreads();
+  for (int v = 0; v < warp; ++v) mex = max(mex, wmx[v]);
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    if (FULL || k0 + q < P) {
+      const int i = max(mex, r[q]);
+      s.px[q] = st[i];
+      s.py[q] = st[P + i];
+      s.vx[q] = st[2 * P + i];
+      s.vy[q] = st[3 * P + i];
+      s.w[q] = inv_n;
+    }
+  }
+  // S.st / S.cum are next written after this set's estimate barrier
 }
 
 // Issue the TMA prefetch of particle set g (5 fields x P doubles) into S.pf.
@@ -753,7 +784,7 @@ __device__ __forceinline__ void prefetch_set(const DevBatch& B, const Smem& S, i
 // finalize (env.cpp:397-409) for set (a, t) of env e (global set index gset).
 // FULL (P == blockDim * PPT, P % 4 == 0): the set arrives in S.pf by TMA
 // (phase `tphase`), the Philox blocks are computed in registers and the next
-// set `next` (>= 0) is prefetched right after the set-start barrier.
+// set `next` (>= 0) is prefetched once every thread has read this one.
 template <int PPT, bool FULL>
 __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, const Rec& rec,
                          int64_t gi, int64_t gset, int a, int t, uint32_t& tphase, int64_t next) {
@@ -762,9 +793,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   const int ps = a * T + t;     // PF stream id / set within the env (env.cpp:130-133)
   const int ti = a * c.sT + t;  // track index in the record
   const int k0 = tid * PPT;
-  uint64_t pos = (uint64_t)TRK(K_POS, ti);
-  const double ms = TRK(K_MAXSPEED, ti);
-  const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)ps);
+  const double* tk = S.trk + kTrkStride * ti;  // staged by stage_env
+  uint64_t pos = (uint64_t)tk[TK_POS];
+  const double ms = tk[TK_MAXSPEED];
+  const uint64_t key = (uint64_t)__double_as_longlong(tk[TK_KEY]);
   const size_t base = (size_t)gset * P;
   const int off = (int)(pos & 3);
   const bool noise = c.noise_on != 0;
@@ -791,20 +823,28 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // ---- Philox words of fill_normals (tracking.cpp:24-37): particle k needs the
   // words at pos + s*P + k for segments s = 0..3. FULL: thread t computes the
   // aligned block (pos/4 + s*P/4 + t) of each segment; a misaligned stream takes
-  // its remaining words from the next lane's block (shuffle) or, for lane 31,
-  // from the next warp's lane 0 / segment s+1 (smem exchange).
+  // its remaining words from the next lane's block (shuffle). Lane 31 needs the
+  // block after its warp's range in each segment: lanes 0..3 of every warp
+  // compute those four as a fifth, interleaved chain (so no warp waits for
+  // another) and hand them over through the warp's xch slots. The last warp's
+  // segment-3 extra block, pos/4 + P, also holds the resample draw at pos + 4P.
   uint4 blk[4];
   if (FULL && noise) {
     const uint64_t b0 = (pos >> 2) + (uint64_t)tid;
+    const uint64_t be = (pos >> 2) + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + (uint64_t)(32 * (warp + 1));
 #pragma unroll
     for (int q = 0; q < 4; ++q) blk[q] = philox(key, (uint64_t)ps, b0 + (uint64_t)q * (uint64_t)(P / 4));
-    if (off != 0 && lane == 0) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) S.xch[warp * 5 + q] = blk[q];
-      if (warp == 0) S.xch[4] = philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P);
+    const uint4 ex = philox(key, (uint64_t)ps, be);
+    if (lane < 4) S.xch[warp * 5 + lane] = ex;
+    if (warp == nw - 1 && lane == 3) {
+      const uint4 y = off == 3 ? philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P + 1) : ex;
+      uint32_t w2[4];
+      words_at(ex, y, off, w2);
+      reinterpret_cast<uint32_t*>(S.bc)[0] = w2[0];
+      reinterpret_cast<uint32_t*>(S.bc)[1] = w2[1];
     }
-  }
-  if (tid == 0) {  // the resample draw, broadcast through smem
+    __syncwarp();
+  } else if (tid == 0) {  // the resample draw, broadcast through smem
     const uint4 x = philox(key, (uint64_t)ps, u0p >> 2);
     const int o = (int)(u0p & 3);
     const uint4 y = o == 3 ? philox(key, (uint64_t)ps, (u0p >> 2) + 1) : x;
@@ -813,9 +853,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     reinterpret_cast<uint32_t*>(S.bc)[0] = w2[0];
     reinterpret_cast<uint32_t*>(S.bc)[1] = w2[1];
   }
-  __syncthreads();  // set-start barrier: xch / u0 published
-  const uint64_t u0_lo = reinterpret_cast<const uint32_t*>(S.bc)[0];
-  const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
+  // S.bc is read before the resample, after at least one block barrier; the
+  // previous set's reads of it precede its estimate barrier.
 
   // ---- pf::predict (tracking.cpp:94-117): the normals first
   float zpx[PPT], zpy[PPT], zvx[PPT], zvy[PPT];  // out[k], out[P+k], out[2P+k], out[3P+k]
@@ -828,7 +867,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         nb.x = __shfl_down_sync(0xffffffffu, blk[q].x, 1);
         nb.y = __shfl_down_sync(0xffffffffu, blk[q].y, 1);
         nb.z = __shfl_down_sync(0xffffffffu, blk[q].z, 1);
-        if (off != 0 && lane == 31) nb = warp + 1 < nw ? S.xch[(warp + 1) * 5 + q] : S.xch[q + 1];
+        if (off != 0 && lane == 31) nb = S.xch[warp * 5 + q];
         words_at(blk[q], nb, off, W[q]);
       }
     } else {
@@ -839,17 +878,23 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           W[q][j] = k0 + j < P ? word_at(key, (uint64_t)ps, pos + (uint64_t)q * (uint64_t)P + (uint64_t)(k0 + j)) : 0u;
     }
     // pair k: u1 = word(pos+k), u2 = word(pos+2P+k); pair P+k: segments 1, 3
-    bool ok = true;
+    uint32_t bad = 0;  // pairs with an uncertain rounding: exact fp64 libm path
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      ok &= box_muller_fast(W[0][j], W[2][j], S.tab_log, S.tab_sc, zpx[j], zvx[j]);
-      ok &= box_muller_fast(W[1][j], W[3][j], S.tab_log, S.tab_sc, zpy[j], zvy[j]);
+      bad |= box_muller_fast(W[0][j], W[2][j], S.tab_log, S.tab_sc, zpx[j], zvx[j]) ? 0u : 1u << (2 * j);
+      bad |= box_muller_fast(W[1][j], W[3][j], S.tab_log, S.tab_sc, zpy[j], zvy[j]) ? 0u : 2u << (2 * j);
     }
-    if (!ok) {  // an uncertain rounding (p ~ 1e-4 per particle): exact fp64 libm path
-#pragma unroll 1
+    if (bad) {
+#pragma unroll
       for (int j = 0; j < PPT; ++j) {
-        box_muller_slow(W[0][j], W[2][j], zpx[j], zvx[j]);
-        box_muller_slow(W[1][j], W[3][j], zpy[j], zvy[j]);
+        if (bad & (1u << (2 * j))) {
+          const float2 z = box_muller_slow(W[0][j], W[2][j]);
+          zpx[j] = z.x, zvx[j] = z.y;
+        }
+        if (bad & (2u << (2 * j))) {
+          const float2 z = box_muller_slow(W[1][j], W[3][j]);
+          zpy[j] = z.x, zvy[j] = z.y;
+        }
       }
     }
     pos += 4ull * (uint64_t)P;
@@ -941,7 +986,14 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll 1
     for (int j = 0; j < nm; ++j) {
       float sj = mb[j * 32];
-      for (int v = 1; v < nw; ++v) sj = fmaxf(sj, mb[j * 32 + v]);
+      if ((nw & 3) == 0) {
+        for (int v = 0; v < nw; v += 4) {
+          const float4 m4 = *reinterpret_cast<const float4*>(mb + j * 32 + v);
+          sj = fmaxf(fmaxf(sj, m4.x), fmaxf(m4.y, fmaxf(m4.z, m4.w)));
+        }
+      } else {
+        for (int v = 1; v < nw; ++v) sj = fmaxf(sj, mb[j * 32 + v]);
+      }
       shift = j == 0 ? (double)sj : shift + (double)sj;
     }
     if (!isfinite(shift)) {
@@ -997,7 +1049,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // so the reference's recomputation cannot resample: skipped unless the state
   // was injected.
   bool resampled = false;
-  const bool ess_known_ok = nm == 0 && TRK(K_ESSOK, ti) != 0.0;
+  const bool ess_known_ok = nm == 0 && tk[TK_ESSOK] != 0.0;
   if (!ess_known_ok) {
     if (!have_ess) {
       double w2 = 0.0;
@@ -1006,6 +1058,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       ess = 1.0 / R.sum(w2);
     }
     if (ess < (double)P / 2.0) {
+      const uint64_t u0_lo = reinterpret_cast<const uint32_t*>(S.bc)[0];
+      const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
       const double u0 = (double)(((u0_hi << 32) | u0_lo) >> 11) * 0x1.0p-53;
       pos += 2;
       pf_resample<PPT, FULL>(s, k0, P, u0, S);
@@ -1019,7 +1073,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
            (unsigned long long)pos);
 
   // ---- estimate (env.cpp:403-407)
-  const double3 est = pf_estimate<PPT, FULL>(s, k0, P, TRK(K_EX, ti), TRK(K_EY, ti), R);
+  const double3 est = pf_estimate<PPT, FULL>(s, k0, P, tk[TK_EX], tk[TK_EY], R);
   if (FULL) {
 #pragma unroll
     for (int q = 0; q < PPT; q += 2) {
@@ -1046,8 +1100,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     TRK(K_EX, ti) = est.x;
     TRK(K_EY, ti) = est.y;
     TRK(K_SPREAD, ti) = est.z;
-    TRK(K_AGE, ti) = fresh ? 0.0 : TRK(K_AGE, ti) + 1.0;
-    TRK(K_EVER, ti) = (TRK(K_EVER, ti) != 0.0 || fresh) ? 1.0 : 0.0;
+    TRK(K_AGE, ti) = fresh ? 0.0 : tk[TK_AGE] + 1.0;
+    TRK(K_EVER, ti) = (tk[TK_EVER] != 0.0 || fresh) ? 1.0 : 0.0;
     TRK(K_POS, ti) = (double)pos;
     TRK(K_ESSOK, ti) = 1.0;  // maybe_resample ran: ESS >= P/2 or weights uniform
     STAT(7) += (double)nm;
@@ -1081,6 +1135,16 @@ __device__ __forceinline__ void stage_env(const DevConfig& cg, const DevBatch& B
     for (int s = 0; s < A; ++s)
       if (s != a && link[a * sA + s] && present[s * sT + t]) ml[n++] = (uint16_t)(s * sT + t);
     S.mcount[ti] = (uint16_t)n;
+    double* tk = S.trk + kTrkStride * ti;
+    tk[TK_POS] = TRK(K_POS, ti);
+    tk[TK_MAXSPEED] = TRK(K_MAXSPEED, ti);
+    tk[TK_EX] = TRK(K_EX, ti);
+    tk[TK_EY] = TRK(K_EY, ti);
+    tk[TK_ESSOK] = TRK(K_ESSOK, ti);
+    tk[TK_AGE] = TRK(K_AGE, ti);
+    tk[TK_EVER] = TRK(K_EVER, ti);
+    tk[TK_KEY] = __longlong_as_double((long long)derive_key(B.seed, kTagPf, (uint64_t)(B.env_index_offset + e),
+                                                            (uint64_t)(a * T + t)));
   }
 }
 
