@@ -1,0 +1,35 @@
+// Exercises include/ut_vecenv.hpp the way reference-side C++ would use
+// utrack::VecEnv (test_vecenv.cpp style). Prints one JSON line.
+#include <cstdio>
+#include <vector>
+
+#include "ut_vecenv.hpp"
+
+namespace ut = utrack_b200;
+
+int main() {
+  try {
+    ut::EnvConfig cfg = ut::default_config();
+    cfg.n_agents = 2;
+    cfg.n_targets = 2;
+    cfg.pf.n_particles = 64;
+    cfg.horizon = 3;
+    ut::VecEnv venv(cfg, 4, 7);
+    std::vector<int> acts(static_cast<size_t>(venv.n_envs() * venv.n_agents()), 2);  // hold course
+    venv.step(acts);
+    venv.step_policy(ut::BenchmarkPolicy::kRandom);
+    venv.step(acts);
+    double rsum = 0.0;
+    for (double r : venv.rewards()) rsum += r;
+    int done = 0;
+    for (auto d : venv.dones()) done += d;
+    std::printf("{\"ok\": 1, \"reward_sum\": %.17g, \"dones\": %d, \"obs00\": %.17g, \"step0\": %d, \"blob\": %zu}\n",
+                rsum, done, venv.obs_stack()(0, 0), venv.world_step(0), venv.serialize_state(0).size());
+  } catch (const ut::DeviceError& e) {
+    std::printf("{\"ok\": 0, \"error\": \"DeviceError\"}\n");
+  } catch (const std::exception& e) {
+    std::printf("{\"ok\": 0, \"error\": \"%s\"}\n", e.what());
+    return 1;
+  }
+  return 0;
+}
