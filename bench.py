@@ -117,6 +117,27 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def workload_config(name, per_gpu, total, particles):
+    """The `config` object both arms print (same workload, same keys)."""
+    c = CONFIGS[name]
+    A, T = c["n_agents"], c["n_targets"]
+    gb = algorithmic_bytes_per_env_step(A, T, particles, rec_words_for(A, T)) * per_gpu / 1e9
+    return {"workload": f"{name}: {c['desc']}", "envs_per_gpu": per_gpu, "total_envs": total,
+            "particles": particles, "agents": A, "targets": T,
+            "policy": "random legal (bench stream, vecenv.cpp:125-134)",
+            "l2": f"inputs larger than L2 ({gb:.1f} GB touched per step per GPU)"}
+
+
+def measured_traffic(name, per_gpu, particles):
+    """DRAM bytes per step-kernel launch from the committed ncu --set full capture
+    of the same workload (profiles/traffic.json), or None."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text()).get(f"{name}:{per_gpu}:{particles}")
+    return None if d is None else float(d["dram_bytes_per_launch"])
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -175,12 +196,13 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     base = cpu_baseline(args.config, args.particles, budget_s=max(5.0, 2.0 * (args.steps + args.warmup)))
+    per_gpu = args.envs_per_gpu or CONFIGS[args.config]["envs"]
     line = {
         "metric": "agent-env steps/sec (5v5 fast targets)" if args.config == "c3" else f"agent-env steps/sec ({args.config})",
         "value": base["value"], "unit": "agent-env steps/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}", "particles": args.particles},
+        "config": workload_config(args.config, per_gpu, per_gpu * args.gpus, args.particles),
         "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "agent-env steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -307,17 +329,15 @@ def main():
         "value": value, "unit": "agent-env steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {CONFIGS[args.config]['desc']}", "envs_per_gpu": per_gpu,
-                   "total_envs": total, "particles": P, "agents": A, "targets": T,
-                   "policy": "device random legal (bench stream, vecenv.cpp:125-134)",
-                   "l2": f"inputs larger than L2 ({bytes_launch / 1e9:.1f} GB touched per step per GPU)",
-                   "env_steps_per_s": env_steps / secs},
+        "config": dict(workload_config(args.config, per_gpu, total, P), env_steps_per_s=env_steps / secs),
         "e2e": {"value": e2e_value, "unit": "agent-env steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "path": "VecEnv.step(host int32 actions) + copy_outputs to pinned host (ut_vecenv_step + ut_vecenv_copy_outputs)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": args.traffic_bytes,
-                     "kernel": "step_kernel<4>", "bytes_per_launch": bytes_launch,
+                     "frac": achieved / peak,
+                     "traffic": args.traffic_bytes if args.traffic_bytes is not None
+                     else measured_traffic(args.config, per_gpu, P),
+                     "kernel": "step_kernel<4,1024,FULL>", "bytes_per_launch": bytes_launch,
                      "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_kind},
         "gpu_launches": gpu_launches,
         "clocks": clocks.summary(),

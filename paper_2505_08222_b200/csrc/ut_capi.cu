@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -206,9 +207,14 @@ struct ut_vecenv {
   int np = 1024;              // particle capacity of the step kernel instance
   size_t smem_reset = 0;      // the reset kernel always uses the 1024 layout
 
+  int ppt = kPPT;              // particles per thread of the step kernel (2: 512-thread CTAs)
+  int nt_reset = 0;
+
   int launch_step(int mode) {
     const dim3 g((unsigned)grid), b((unsigned)nt);
-    if (full && np == 1024)
+    if (full && np == 1024 && ppt == 2)
+      step_kernel<2, 1024, true><<<g, b, smem, stream>>>(B, mode, d_status);
+    else if (full && np == 1024)
       step_kernel<kPPT, 1024, true><<<g, b, smem, stream>>>(B, mode, d_status);
     else if (full && np == 512)
       step_kernel<kPPT, 512, true><<<g, b, smem, stream>>>(B, mode, d_status);
@@ -221,7 +227,7 @@ struct ut_vecenv {
     return UT_OK;
   }
   int launch_reset(int ctor) {
-    reset_kernel<kPPT, 1024><<<(unsigned)grid, nt, smem_reset, stream>>>(B, ctor, d_status);
+    reset_kernel<kPPT, 1024><<<(unsigned)grid, nt_reset, smem_reset, stream>>>(B, ctor, d_status);
     ++launches;
     UT_CUDA(cudaGetLastError());
     return UT_OK;
@@ -337,7 +343,7 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   UT_CUDA(cudaMemsetAsync(acts, 0, sizeof(int32_t) * n_envs * Am, v->stream));
   UT_CUDA(cudaMemsetAsync(B.sched_flags, 0, n_envs * (Am * Tm + Am * Am), v->stream));
 
-  v->nt = threads_for(v->P);
+  v->nt = v->nt_reset = threads_for(v->P);
   int max_optin = 0, sms = 0;
   UT_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -345,7 +351,13 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   v->full = (v->P == v->nt * kPPT) && (v->P == 1024 || v->P == 512 || v->P == 256);
   v->np = v->full ? v->P : 1024;
   const void* fn = nullptr;
-  if (v->np == 1024 && v->full) {
+  const char* ppt_env = getenv("UT_DEBUG_PPT");
+  if (v->full && v->P == 1024 && ppt_env && atoi(ppt_env) == 2) {
+    v->ppt = 2;
+    v->nt = 512;
+    fn = (const void*)step_kernel<2, 1024, true>;
+    v->smem = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
+  } else if (v->np == 1024 && v->full) {
     fn = (const void*)step_kernel<kPPT, 1024, true>;
     v->smem = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
   } else if (v->np == 512) {
@@ -358,7 +370,7 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
     fn = (const void*)step_kernel<kPPT, 1024, false>;
     v->smem = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
   }
-  v->smem_reset = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
+  v->smem_reset = smem_bytes<1024>(v->A_max, v->T_max, v->nt_reset);
   if ((int)v->smem_reset > max_optin)
     return fail(UT_ERR_CONFIG, "configuration needs %zu B of shared memory per CTA (max %d)", v->smem_reset, max_optin);
   UT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
@@ -368,6 +380,8 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   int per_sm = 0;
   UT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v->nt, v->smem));
   if (per_sm < 1) return fail(UT_ERR_RUNTIME, "step kernel cannot be resident with %zu B shared memory", v->smem);
+  // debug knob (occupancy experiments): cap resident CTAs per SM
+  if (const char* cap = getenv("UT_DEBUG_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(cap)));
   v->grid = (int)std::min<int64_t>(n_envs, (int64_t)per_sm * sms);
   if ((rc = v->alloc(&v->d_self, 1))) return rc;
   if ((rc = v->sync_batch())) return rc;

@@ -28,7 +28,7 @@ namespace ut {
 enum StepMode : int { MODE_EXTERNAL = -1, MODE_RANDOM = 0, MODE_SCRIPTED = 1 };
 enum DevStatus : int { ST_OK = 0, ST_SPAWN_INFEASIBLE = 2 };
 constexpr int kMaxMerged = 8;     // merged update handles up to 8 measurements per set
-constexpr int kMeasStride = 8;    // ox, oy, r2, sigma, 1/sigma (+pad)
+constexpr int kMeasStride = 8;    // ox, oy, r2, sigma, -1/(2 sigma^2) (+pad)
 constexpr int kMaxEntities = 64;  // spawn scratch per thread
 constexpr double kMergeFloor = 0x1p-860;  // see the merged-update argument in step_set
 constexpr int kChunkFlagDone = 1, kChunkFlagSpawned = 2;
@@ -629,7 +629,7 @@ __device__ __noinline__ int pf_update_seq(const double* m, int k0, int P, const 
 // previous estimate (cx, cy), mean = c + sum w (p - c), spread^2 = second moment
 // minus the squared shift; exact second pass when that subtraction could lose
 // more than ~1e-11 relative.
-template <int PPT, bool FULL>
+template <int PPT, bool FULL, int NW>
 __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, int P, double cx, double cy,
                                                BlockReducer& R) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -642,7 +642,7 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
       a2 = a2 + s.w[j] * (dx * dx + dy * dy);
     }
   }
-  const double3 m = R.sum3(a0, a1, a2);
+  const double3 m = R.sum3<NW>(a0, a1, a2);
   const double mx = cx + m.x, my = cy + m.y;
   const double shift2 = m.x * m.x + m.y * m.y;
   const double var = m.z - shift2;
@@ -655,13 +655,13 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
       acc = acc + s.w[j] * (dx * dx + dy * dy);
     }
   }
-  return make_double3(mx, my, sqrt(R.sum(acc)));
+  return make_double3(mx, my, sqrt(R.sum<NW>(acc)));
 }
 
 // pf::resample (tracking.cpp:147-170): inclusive scan of w in index order, then
 // output j takes the first particle whose cumulative weight reaches (j + u0)/n,
 // clamped to n - 1 (the reference's monotone two-pointer walk).
-template <int PPT, bool FULL>
+template <int PPT, bool FULL, int NW>
 __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Smem& S) {
   const int tid = threadIdx.x;
   int* mark = reinterpret_cast<int*>(S.cum);  // [P] first output of each particle
@@ -702,9 +702,18 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   // cum[k] = base + loc[q] (the scan's values); cum[k0 - 1] exactly as the
   // previous thread computes it
   double woff = 0.0, woff_prev = 0.0;
-  for (int v = 0; v < warp; ++v) {
-    woff_prev = woff;
-    woff = woff + wsum[v];
+  if constexpr (NW > 0) {
+#pragma unroll
+    for (int v = 0; v < NW - 1; ++v)
+      if (v < warp) {
+        woff_prev = woff;
+        woff = woff + wsum[v];
+      }
+  } else {
+    for (int v = 0; v < warp; ++v) {
+      woff_prev = woff;
+      woff = woff + wsum[v];
+    }
   }
   const double base = woff + excl;
   double c[PPT];
@@ -720,8 +729,10 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   auto count_le = [&](double cv) -> int {
     const double x = cv * (double)P - u0;
     int m = x < 0.0 ? 0 : (x >= (double)P ? P : (int)x + 1);
-    while (m > 0 && ((double)(m - 1) + u0) * inv_n > cv) --m;
-    while (m < P && ((double)m + u0) * inv_n <= cv) ++m;
+    // x is within ~1e-12 of the real boundary and each u_j within an ulp of
+    // (j + u0)/n, so the estimate is off by at most one either way
+    if (m > 0 && ((double)(m - 1) + u0) * inv_n > cv) --m;
+    if (m < P && ((double)m + u0) * inv_n <= cv) ++m;
     return m;
   };
   int lo = tid == 0 ? 0 : count_le(cprev);
@@ -752,7 +763,13 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   int* wmx = reinterpret_cast<int*>(wsum + 96);
   if (lane == 31) wmx[warp] = mi;
   __syncthreads();
-  for (int v = 0; v < warp; ++v) mex = max(mex, wmx[v]);
+  if constexpr (NW > 0) {
+#pragma unroll
+    for (int v = 0; v < NW - 1; ++v)
+      if (v < warp) mex = max(mex, wmx[v]);
+  } else {
+    for (int v = 0; v < warp; ++v) mex = max(mex, wmx[v]);
+  }
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     if (FULL || k0 + q < P) {
@@ -785,7 +802,7 @@ __device__ __forceinline__ void prefetch_set(const DevBatch& B, const Smem& S, i
 // FULL (P == blockDim * PPT, P % 4 == 0): the set arrives in S.pf by TMA
 // (phase `tphase`), the Philox blocks are computed in registers and the next
 // set `next` (>= 0) is prefetched once every thread has read this one.
-template <int PPT, bool FULL>
+template <int PPT, bool FULL, int NW>
 __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, const Rec& rec,
                          int64_t gi, int64_t gset, int a, int t, uint32_t& tphase, int64_t next) {
   const int P = c.P, tid = threadIdx.x, T = c.T;
@@ -829,7 +846,31 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // another) and hand them over through the warp's xch slots. The last warp's
   // segment-3 extra block, pos/4 + P, also holds the resample draw at pos + 4P.
   uint4 blk[4];
-  if (FULL && noise) {
+  if (FULL && noise && PPT == 2) {
+    // PPT = 2 (512 threads): a warp's 64 particles use blocks [16w, 16w + 16] of
+    // each segment. Lane pair (2m, 2m+1) computes block 16w + m of segments
+    // {0, 1} / {2, 3}, lanes 0..3 block 16w + 16 of segment lane as a third
+    // chain; all 68 land in the warp's staging slots (the resample area, free
+    // until this set's update) in segment-major word order, so particle k's word
+    // for segment q sits at word q*68 + off + (k - 64w).
+    uint4* stg = reinterpret_cast<uint4*>(S.st) + warp * 68;
+    const uint64_t wb = (pos >> 2) + (uint64_t)(16 * warp);
+    const int m = lane >> 1, qa = (lane & 1) * 2;
+    const uint4 b0 = philox(key, (uint64_t)ps, wb + (uint64_t)qa * (uint64_t)(P / 4) + (uint64_t)m);
+    const uint4 b1 = philox(key, (uint64_t)ps, wb + (uint64_t)(qa + 1) * (uint64_t)(P / 4) + (uint64_t)m);
+    const uint4 ex = philox(key, (uint64_t)ps, wb + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + 16u);
+    stg[qa * 17 + m] = b0;
+    stg[(qa + 1) * 17 + m] = b1;
+    if (lane < 4) stg[lane * 17 + 16] = ex;
+    if (warp == nw - 1 && lane == 3) {
+      const uint4 y = off == 3 ? philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P + 1) : ex;
+      uint32_t w2[4];
+      words_at(ex, y, off, w2);
+      reinterpret_cast<uint32_t*>(S.bc)[0] = w2[0];
+      reinterpret_cast<uint32_t*>(S.bc)[1] = w2[1];
+    }
+    __syncwarp();
+  } else if (FULL && noise) {
     const uint64_t b0 = (pos >> 2) + (uint64_t)tid;
     const uint64_t be = (pos >> 2) + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + (uint64_t)(32 * (warp + 1));
 #pragma unroll
@@ -859,16 +900,24 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // ---- pf::predict (tracking.cpp:94-117): the normals first
   float zpx[PPT], zpy[PPT], zvx[PPT], zvy[PPT];  // out[k], out[P+k], out[2P+k], out[3P+k]
   if (noise) {
-    uint32_t W[4][4];  // [segment][particle]
-    if (FULL) {
+    uint32_t W[4][PPT];  // [segment][particle]
+    if (FULL && PPT == 2) {
+      const uint32_t* sw = reinterpret_cast<const uint32_t*>(S.st) + warp * 68 * 4 + off + 2 * lane;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 nb;
-        nb.x = __shfl_down_sync(0xffffffffu, blk[q].x, 1);
-        nb.y = __shfl_down_sync(0xffffffffu, blk[q].y, 1);
-        nb.z = __shfl_down_sync(0xffffffffu, blk[q].z, 1);
-        if (off != 0 && lane == 31) nb = S.xch[warp * 5 + q];
-        words_at(blk[q], nb, off, W[q]);
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) W[q][j] = sw[q * 68 + j];
+    } else if (FULL) {
+      if constexpr (PPT == 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 nb;
+          nb.x = __shfl_down_sync(0xffffffffu, blk[q].x, 1);
+          nb.y = __shfl_down_sync(0xffffffffu, blk[q].y, 1);
+          nb.z = __shfl_down_sync(0xffffffffu, blk[q].z, 1);
+          if (off != 0 && lane == 31) nb = S.xch[warp * 5 + q];
+          words_at(blk[q], nb, off, W[q]);
+        }
       }
     } else {
 #pragma unroll
@@ -964,15 +1013,15 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll 1
     for (int j = 0; j < nm; ++j) {
       const double* m = S.meas + kMeasStride * ml[j];
-      const double ox = m[0], oy = m[1], r2 = m[2], sig = m[3], rsig = m[4];
+      const double ox = m[0], oy = m[1], r2 = m[2], c2 = m[4];
       float mj = -CUDART_INF_F;
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         if (FULL || k0 + q < P) {
           const double dx = s.px[q] - ox, dy = s.py[q] - oy;
           const double d = sqrt_dist(dx * dx + dy * dy);
-          const double qv = div_rcp(d - r2, sig, rsig);
-          const double ll = 0.0 - 0.5 * (qv * qv);
+          const double tq = d - r2;
+          const double ll = (tq * tq) * c2;  // -(1/2)((d - r)/sigma)^2 to a few ulp
           L[q] = L[q] + ll;
           mj = fmaxf(mj, __double2float_ru(ll));
         }
@@ -986,8 +1035,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll 1
     for (int j = 0; j < nm; ++j) {
       float sj = mb[j * 32];
-      if ((nw & 3) == 0) {
-        for (int v = 0; v < nw; v += 4) {
+      if constexpr (NW > 0 && NW % 4 == 0) {
+#pragma unroll
+        for (int v = 0; v < NW; v += 4) {
           const float4 m4 = *reinterpret_cast<const float4*>(mb + j * 32 + v);
           sj = fmaxf(fmaxf(sj, m4.x), fmaxf(m4.y, fmaxf(m4.z, m4.w)));
         }
@@ -1011,7 +1061,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           lx = max(lx, __double2hiint(e[q]) >> 20);
         }
       }
-      const double2 r = R.sum2_imax(ls, lq, lx);
+      const double2 r = R.sum2_imax<NW>(ls, lq, lx);
       if (isfinite(r.x) && r.x > 0.0 && lx >= 1023 - 860) {  // max(e) >= 2^-860
         const double rcp = 1.0 / r.x;
 #pragma unroll
@@ -1055,14 +1105,14 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       double w2 = 0.0;
 #pragma unroll
       for (int q = 0; q < PPT; ++q) w2 = w2 + s.w[q] * s.w[q];
-      ess = 1.0 / R.sum(w2);
+      ess = 1.0 / R.sum<NW>(w2);
     }
     if (ess < (double)P / 2.0) {
       const uint64_t u0_lo = reinterpret_cast<const uint32_t*>(S.bc)[0];
       const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
       const double u0 = (double)(((u0_hi << 32) | u0_lo) >> 11) * 0x1.0p-53;
       pos += 2;
-      pf_resample<PPT, FULL>(s, k0, P, u0, S);
+      pf_resample<PPT, FULL, NW>(s, k0, P, u0, S);
       resampled = true;
     }
   }
@@ -1073,7 +1123,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
            (unsigned long long)pos);
 
   // ---- estimate (env.cpp:403-407)
-  const double3 est = pf_estimate<PPT, FULL>(s, k0, P, tk[TK_EX], tk[TK_EY], R);
+  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R);
   if (FULL) {
 #pragma unroll
     for (int q = 0; q < PPT; q += 2) {
@@ -1128,7 +1178,7 @@ __device__ __forceinline__ void stage_env(const DevConfig& cg, const DevBatch& B
     m[1] = AG(V_Y, a);
     m[2] = r2[ti];
     m[3] = c.sigma_meas;
-    m[4] = 1.0 / c.sigma_meas;
+    m[4] = -0.5 / (c.sigma_meas * c.sigma_meas);
     int n = 0;
     uint16_t* ml = S.mlist + ti * sA;
     if (present[ti]) ml[n++] = (uint16_t)ti;
@@ -1191,7 +1241,7 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
     }
   }
   pos += 8ull * (uint64_t)P;
-  const double3 est = pf_estimate<PPT, false>(s, k0, P, cx, cy, R);
+  const double3 est = pf_estimate<PPT, false, 0>(s, k0, P, cx, cy, R);
   const size_t base = (size_t)gset * P;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
@@ -1244,7 +1294,8 @@ __device__ __noinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t
 
 // The fused step.
 template <int PPT, int NP, bool FULL>
-__global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode, int32_t* status) {
+__global__ void __launch_bounds__(PPT == 2 ? 512 : 256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode,
+                                                                                       int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem S = carve<NP>(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT);
   const DevBatch& Bg = *B.self;  // cold paths read the global copy
@@ -1280,7 +1331,8 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
       for (int a = 0; a < c.A; ++a)
         for (int t = 0; t < c.T; ++t) {
           const int64_t g = so + a * c.T + t;
-          step_set<PPT, FULL>(c, B, S, R, rec, gi, g, a, t, tphase, g + 1 < set_end ? g + 1 : -1);
+          step_set<PPT, FULL, FULL ? NP / (32 * PPT) : 0>(c, B, S, R, rec, gi, g, a, t, tphase,
+                                                           g + 1 < set_end ? g + 1 : -1);
         }
       __syncthreads();  // S.cfg / meas / mlist reused by the next env
     }
