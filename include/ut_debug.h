@@ -7,9 +7,11 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
-/* Evaluates the device's fp32 noise transcendental on its whole 2^24-point input
- * grid (tracking.cpp:29-36): kind 0 = log(((i)+1) * 2^-24), 1 = cos(2pi_f * i*2^-24),
- * 2 = sin(2pi_f * i*2^-24). host_out receives 2^24 floats. */
+/* Evaluates the device's fp32 noise math on its whole 2^24-point input grid
+ * (tracking.cpp:29-36): quantity q = kind % 4: 0 = log(((i)+1) * 2^-24),
+ * 1 = cos(2pi_f * i*2^-24), 2 = sin(2pi_f * i*2^-24), 3 = sqrt(-2 log(((i)+1) * 2^-24));
+ * kind 0..3 through the fp64-libm path, 4..7 through the table-driven production
+ * path. host_out receives 2^24 floats. */
 int ut_debug_cr_grid(int kind, int device, float* host_out);
 /* n consecutive Philox4x32-10 blocks from block0 (rng.hpp:116-131): 4n words. */
 int ut_debug_philox(uint64_t key, uint64_t stream, uint64_t block0, int32_t n, int device, uint32_t* host_out);

@@ -167,8 +167,9 @@ float uto_cr_sinf(float x) { return (float)sin((double)x); }
 void uto_cr_grid(int kind, float* out) {
   const float two_pi_f = 2.0f * (float)UTO_PI;
   for (uint32_t i = 0; i < (1u << 24); ++i) {
-    if (kind == 0) {
-      out[i] = uto_cr_logf((float)(i + 1u) * 0x1.0p-24f);
+    if (kind == 0 || kind == 3) {
+      const float l = uto_cr_logf((float)(i + 1u) * 0x1.0p-24f);
+      out[i] = kind == 0 ? l : sqrtf(-2.0f * l);
     } else {
       const float a = two_pi_f * ((float)i * 0x1.0p-24f);
       out[i] = kind == 1 ? uto_cr_cosf(a) : uto_cr_sinf(a);

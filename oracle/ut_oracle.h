@@ -40,6 +40,7 @@ uint64_t uto_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t d);
 float uto_cr_logf(float x);
 float uto_cr_cosf(float x);
 float uto_cr_sinf(float x);
+/* kind 0 log, 1 cos, 2 sin, 3 sqrt(-2 log) over the 2^24 draw grid (ut_debug.h) */
 void uto_cr_grid(int kind, float* out);
 /* fills out[0..4n) with the predict noise of one particle set starting at u32
  * stream position `pos` (tracking.cpp:24-37) */

@@ -817,21 +817,24 @@ int ut_benchmark_sps(const ut_env_config* cfg, int64_t n_envs, int32_t n_steps, 
 
 // ------------------------------------------------------------ ut_debug.h ---
 namespace {
-__global__ void cr_grid_kernel(int kind, float* out) {
+// Grid quantity q: 0 log(u1), 1 cos(2pi_f u2), 2 sin(2pi_f u2), 3 the Box-Muller
+// radius sqrt(-2 log u1), over all 2^24 values the 24-bit draws can produce.
+__global__ void cr_grid_kernel(int q, float* out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (1u << 24)) return;
   const float two_pi_f = 2.0f * 3.14159265358979323846f;
-  if (kind == 0) {
-    out[i] = cr_logf((float)(i + 1u) * 0x1.0p-24f);
+  if (q == 0 || q == 3) {
+    const float l = cr_logf((float)(i + 1u) * 0x1.0p-24f);
+    out[i] = q == 0 ? l : __fsqrt_rn(-2.0f * l);
   } else {
     float s, c;
     cr_sincosf(__fmul_rn(two_pi_f, (float)i * 0x1.0p-24f), &s, &c);
-    out[i] = kind == 1 ? c : s;
+    out[i] = q == 1 ? c : s;
   }
 }
-// The production (table-driven) path: fills both grids' results through
-// box_muller_fast, falling back exactly like the step kernel does.
-__global__ void cr_grid_fast_kernel(int kind, float* out) {
+// The production (table-driven) path: the same functions box_muller_fast is
+// built from, falling back exactly like the step kernel does.
+__global__ void cr_grid_fast_kernel(int q, float* out) {
   __shared__ double2 tl[128], ts[64];
   for (int i = threadIdx.x; i < 128; i += blockDim.x) tl[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
   for (int i = threadIdx.x; i < 64; i += blockDim.x) ts[i] = make_double2(kSinCosTab[2 * i], kSinCosTab[2 * i + 1]);
@@ -839,12 +842,13 @@ __global__ void cr_grid_fast_kernel(int kind, float* out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (1u << 24)) return;
   const float two_pi_f = 2.0f * 3.14159265358979323846f;
-  if (kind == 0) {
-    out[i] = cr_logf_fast((float)(i + 1u) * 0x1.0p-24f, tl);
+  if (q == 0 || q == 3) {
+    const float l = cr_logf_fast((float)(i + 1u) * 0x1.0p-24f, tl);
+    out[i] = q == 0 ? l : sqrt_rn_f(-2.0f * l);
   } else {
     float s, c;
     cr_sincosf_fast(__fmul_rn(two_pi_f, (float)i * 0x1.0p-24f), &s, &c, ts);
-    out[i] = kind == 1 ? c : s;
+    out[i] = q == 1 ? c : s;
   }
 }
 __global__ void philox_kernel(uint64_t key, uint64_t stream, uint64_t block0, int n, uint4* out) {
@@ -876,10 +880,11 @@ int ut_debug_cr_grid(int kind, int device, float* host_out) {
   float* d = nullptr;
   const size_t n = (size_t)1 << 24;
   UT_CUDA(cudaMalloc(&d, n * sizeof(float)));
-  if (kind < 3)
+  if (kind < 0 || kind > 7) return fail(UT_ERR_CONTRACT, "cr_grid: kind must be 0..7");
+  if (kind < 4)
     cr_grid_kernel<<<(unsigned)(n / 256), 256>>>(kind, d);
   else
-    cr_grid_fast_kernel<<<(unsigned)(n / 256), 256>>>(kind - 3, d);
+    cr_grid_fast_kernel<<<(unsigned)(n / 256), 256>>>(kind - 4, d);
   cudaError_t err = cudaMemcpy(host_out, d, n * sizeof(float), cudaMemcpyDeviceToHost);
   cudaFree(d);
   UT_CUDA(err);

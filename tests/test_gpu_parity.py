@@ -244,15 +244,16 @@ def test_device_stats_match_oracle(cuda_device):
 
 
 def test_cr_math_exhaustive_on_device(cuda_device):
-    """Device fp32 noise transcendentals == oracle (correctly rounded) on all 3 x 2^24 grid points."""
+    """Device fp32 noise math == oracle (correctly rounded log/cos/sin, IEEE sqrt)
+    on every value the 24-bit draws can produce: 4 x 2^24 grid points."""
     lib = _product()
     o = oracle_lib()
     want = np.empty(1 << 24, np.float32)
     got = np.empty(1 << 24, np.float32)
-    for kind in range(3):
+    for kind in range(4):  # log, cos, sin, Box-Muller radius sqrt(-2 log u1)
         o.uto_cr_grid(kind, want.ctypes.data)
-        # kind: fp64-libm reference path; kind + 3: the table-driven production path
-        for dev_kind in (kind, kind + 3):
+        # kind: fp64-libm reference path; kind + 4: the table-driven production path
+        for dev_kind in (kind, kind + 4):
             assert lib.ut_debug_cr_grid(dev_kind, 0, got.ctypes.data) == 0
             bad = np.flatnonzero(got.view(np.uint32) != want.view(np.uint32))
             assert bad.size == 0, (dev_kind, bad[:10])
