@@ -135,6 +135,8 @@ def declare_debug(lib):
     lib.ut_debug_derive_key.restype = C.c_int
     lib.ut_debug_abi_sizes.argtypes = [C.POINTER(C.c_int64)]
     lib.ut_debug_abi_sizes.restype = C.c_int
+    lib.ut_debug_ieee_check.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int, C.POINTER(C.c_uint64)]
+    lib.ut_debug_ieee_check.restype = C.c_int
     lib.ut_debug_set_knobs.argtypes = [C.c_void_p, C.c_int, C.c_int64]
     lib.ut_debug_set_knobs.restype = C.c_int
     return lib

@@ -851,6 +851,27 @@ __global__ void cr_grid_fast_kernel(int q, float* out) {
     out[i] = q == 1 ? c : s;
   }
 }
+// Random operands over the clamp's domain: sqrt of x = 0 and of log-uniform
+// x in [2^-960, 2^200]; a / b with log-uniform a in [2^-20, 2^20], b >= a.
+__global__ void ieee_check_kernel(int kind, uint64_t seed, int64_t n, unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 r = philox(seed, 0x69656565ull, (uint64_t)i);
+    const double u = ((double)(((uint64_t)r.y << 32 | r.x) >> 11)) * 0x1.0p-53;
+    const double v = ((double)(((uint64_t)r.w << 32 | r.z) >> 11)) * 0x1.0p-53;
+    if (kind == 0) {
+      const double x = i == 0 ? 0.0 : exp2(-960.0 + 1160.0 * u) * (1.0 + v);
+      const double a = sqrt_rn_clamp(x), b = __dsqrt_rn(x);
+      local += __double_as_longlong(a) != __double_as_longlong(b);
+    } else {
+      const double a = exp2(-20.0 + 40.0 * u);
+      const double b = a * (1.0 + 1e6 * v);
+      const double q = div_rn_clamp(a, b), w = __ddiv_rn(a, b);
+      local += __double_as_longlong(q) != __double_as_longlong(w);
+    }
+  }
+  if (local) atomicAdd(bad, local);
+}
 __global__ void philox_kernel(uint64_t key, uint64_t stream, uint64_t block0, int n, uint4* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = philox(key, stream, block0 + (uint64_t)i);
@@ -888,6 +909,19 @@ int ut_debug_cr_grid(int kind, int device, float* host_out) {
   cudaError_t err = cudaMemcpy(host_out, d, n * sizeof(float), cudaMemcpyDeviceToHost);
   cudaFree(d);
   UT_CUDA(err);
+  return UT_OK;
+}
+int ut_debug_ieee_check(int kind, uint64_t seed, int64_t n, int device, uint64_t* mismatches) {
+  UT_CUDA(cudaSetDevice(device));
+  unsigned long long* d = nullptr;
+  UT_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+  UT_CUDA(cudaMemset(d, 0, sizeof(unsigned long long)));
+  ieee_check_kernel<<<1184, 256>>>(kind, seed, n, d);
+  unsigned long long h = 0;
+  cudaError_t err = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  UT_CUDA(err);
+  *mismatches = h;
   return UT_OK;
 }
 int ut_debug_philox(uint64_t key, uint64_t stream, uint64_t block0, int32_t n, int device, uint32_t* host_out) {

@@ -664,9 +664,9 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
 template <int PPT, bool FULL, int NW>
 __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Smem& S) {
   const int tid = threadIdx.x;
-  int* mark = reinterpret_cast<int*>(S.cum);  // [P] first output of each particle
+  int* mark = reinterpret_cast<int*>(S.cum);  // [P] source marks of the outputs
   double* st = S.st;
-  double* wsum = S.red + 2 * kRedSlots;  // [32] warp totals, [32] lane-31 excl, [32] lane-31 run, [32] int maxima
+  double* wsum = S.red + 2 * kRedSlots;  // [32] warp totals, then [32] int warp maxima at +96
   double loc[PPT];
   double run = 0.0;
 #pragma unroll
@@ -690,41 +690,26 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   }
   double excl = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) excl = 0.0;
-  if (lane == 31) {
-    wsum[warp] = incl;
-    wsum[32 + warp] = excl;
-    wsum[64 + warp] = run;
-  }
+  if (lane == 31) wsum[warp] = incl;
 #pragma unroll
   for (int q = 0; q < PPT; ++q)
-    if (FULL || k0 + q < P) mark[k0 + q] = -1;
+    if (FULL || k0 + q < P) mark[k0 + q] = 0;
   __syncthreads();
-  // cum[k] = base + loc[q] (the scan's values); cum[k0 - 1] exactly as the
-  // previous thread computes it
-  double woff = 0.0, woff_prev = 0.0;
+  double woff = 0.0;  // cum[k] = (sum of earlier warps' totals + excl) + loc[q]
   if constexpr (NW > 0) {
 #pragma unroll
     for (int v = 0; v < NW - 1; ++v)
-      if (v < warp) {
-        woff_prev = woff;
-        woff = woff + wsum[v];
-      }
+      if (v < warp) woff = woff + wsum[v];
   } else {
-    for (int v = 0; v < warp; ++v) {
-      woff_prev = woff;
-      woff = woff + wsum[v];
-    }
+    for (int v = 0; v < warp; ++v) woff = woff + wsum[v];
   }
   const double base = woff + excl;
-  double c[PPT];
-#pragma unroll
-  for (int q = 0; q < PPT; ++q) c[q] = base + loc[q];
-  double cprev = __shfl_up_sync(0xffffffffu, c[PPT - 1], 1);
-  if (lane == 0 && warp > 0) cprev = (woff_prev + wsum[32 + warp - 1]) + wsum[64 + warp - 1];
   // Output j takes the first particle i with cum[i] >= u_j, u_j = (j + u0)/n
-  // (clamped to n - 1): particle i owns outputs [count(cum[i-1]), count(cum[i]))
-  // with count(c) = #{j : u_j <= c}; it marks the first one and a prefix max
-  // over the marks hands every output its source.
+  // (clamped to n - 1). With count(c) = #{j : u_j <= c}, the outputs
+  // [count(cum[i-1]), count(cum[i])) are particle i's: particle k marks
+  // count(cum[k]) with k + 1 (the max wins where zero-weight particles share a
+  // boundary) and a prefix max over the marks (0 where unmarked) hands every
+  // output its source; outputs past count(cum[n-2]) fall to n - 1.
   const double inv_n = 1.0 / (double)P;
   auto count_le = [&](double cv) -> int {
     const double x = cv * (double)P - u0;
@@ -735,21 +720,19 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
     if (m < P && ((double)m + u0) * inv_n <= cv) ++m;
     return m;
   };
-  int lo = tid == 0 ? 0 : count_le(cprev);
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     const int k = k0 + q;
-    if (FULL || k < P) {
-      const int hi = k == P - 1 ? P : count_le(c[q]);
-      if (hi > lo) mark[lo] = k;
-      lo = hi;
+    if (k < P - 1) {
+      const int hi = count_le(base + loc[q]);
+      if (hi < P) atomicMax(&mark[hi], k + 1);
     }
   }
   __syncthreads();
   int r[PPT];
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
-    r[q] = (FULL || k0 + q < P) ? mark[k0 + q] : -1;
+    r[q] = (FULL || k0 + q < P) ? mark[k0 + q] : 0;
     if (q > 0) r[q] = max(r[q], r[q - 1]);
   }
   int mi = r[PPT - 1];
@@ -981,8 +964,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   if (ms > 0.0) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
-      const double sp = sqrt(s.vx[j] * s.vx[j] + s.vy[j] * s.vy[j]);
-      const double f = sp > ms ? ms / sp : 1.0;
+      const double sp = sqrt_rn_clamp(s.vx[j] * s.vx[j] + s.vy[j] * s.vy[j]);
+      const double f = sp > ms ? div_rn_clamp(ms, sp) : 1.0;
       s.vx[j] = s.vx[j] * f;
       s.vy[j] = s.vy[j] * f;
     }

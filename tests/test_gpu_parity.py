@@ -276,3 +276,13 @@ def test_philox_and_keys_on_device(cuda_device):
         a, b, c, d = (int(x) for x in rng.integers(0, 2**63, 4, dtype=np.uint64))
         assert lib.ut_debug_derive_key(a, b, c, d, 0, C.byref(out)) == 0
         assert out.value == o.uto_derive_key(a, b, c, d)
+
+
+@pytest.mark.parametrize("kind", [0, 1], ids=["sqrt", "div"])
+def test_speed_clamp_arithmetic_is_ieee(cuda_device, kind):
+    """The branch-free fp64 sqrt / division of the speed clamp == IEEE on 2^28
+    random operands of its domain (the particle state must stay bit-exact)."""
+    lib = _product()
+    bad = C.c_uint64(1)
+    assert lib.ut_debug_ieee_check(kind, 12345, 1 << 28, 0, C.byref(bad)) == 0
+    assert bad.value == 0
