@@ -1,11 +1,15 @@
 """Loader for the in-tree CUDA library. There is no fallback: if the library is
 missing or cannot be loaded, every entry point raises."""
 import ctypes as C
+import os
 import pathlib
 
 from . import _abi
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "libutrack_b200.so"
+# UT_LIBRARY selects another build of the same library (A/B performance runs of
+# in-tree variants under _lib/); unset, the in-tree product library is used.
+LIB_PATH = pathlib.Path(os.environ.get("UT_LIBRARY") or
+                        pathlib.Path(__file__).resolve().parent / "_lib" / "libutrack_b200.so")
 _lib = None
 
 

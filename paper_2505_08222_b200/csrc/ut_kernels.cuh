@@ -1311,9 +1311,10 @@ __global__ void __launch_bounds__(PPT == 2 ? 512 : 256, UT_STEP_MIN_BLOCKS) step
       const DevConfig& c = *S.cfg;
       const int64_t gi = B.env_index_offset + e;
       const int64_t so = set_off(B, e);
-      for (int a = 0; a < c.A; ++a)
-        for (int t = 0; t < c.T; ++t) {
-          const int64_t g = so + a * c.T + t;
+      const int nA = c.A, nT = c.T;
+      for (int a = 0; a < nA; ++a)
+        for (int t = 0; t < nT; ++t) {
+          const int64_t g = so + a * nT + t;
           step_set<PPT, FULL, FULL ? NP / (32 * PPT) : 0>(c, B, S, R, rec, gi, g, a, t, tphase,
                                                            g + 1 < set_end ? g + 1 : -1);
         }
