@@ -567,12 +567,14 @@ __device__ __forceinline__ void gen_words(uint32_t* words, uint64_t key, uint64_
 
 __device__ __forceinline__ void words_at(uint4 x, uint4 y, int off, uint32_t w[4]) {
   // 4 consecutive words starting at lane `off` of block x, continuing into y
-  switch (off) {
-    case 0: w[0] = x.x, w[1] = x.y, w[2] = x.z, w[3] = x.w; break;
-    case 1: w[0] = x.y, w[1] = x.z, w[2] = x.w, w[3] = y.x; break;
-    case 2: w[0] = x.z, w[1] = x.w, w[2] = y.x, w[3] = y.y; break;
-    default: w[0] = x.w, w[1] = y.x, w[2] = y.y, w[3] = y.z; break;
-  }
+  // (branch-free: a 2-word then a 1-word shift of the window)
+  const bool s2 = off & 2, s1 = off & 1;
+  const uint32_t a0 = s2 ? x.z : x.x, a1 = s2 ? x.w : x.y, a2 = s2 ? y.x : x.z, a3 = s2 ? y.y : x.w,
+                 a4 = s2 ? y.z : y.x;
+  w[0] = s1 ? a1 : a0;
+  w[1] = s1 ? a2 : a1;
+  w[2] = s1 ? a3 : a2;
+  w[3] = s1 ? a4 : a3;
 }
 
 // pf::update with one measurement (tracking.cpp:119-143) -- the exact
@@ -855,10 +857,13 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     __syncwarp();
   } else if (FULL && noise) {
     const uint64_t b0 = (pos >> 2) + (uint64_t)tid;
-    const uint64_t be = (pos >> 2) + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + (uint64_t)(32 * (warp + 1));
+    const uint64_t bq[5] = {b0, b0 + (uint64_t)(P / 4), b0 + 2 * (uint64_t)(P / 4), b0 + 3 * (uint64_t)(P / 4),
+                            (pos >> 2) + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + (uint64_t)(32 * (warp + 1))};
+    uint4 bo[5];
+    philox_n<5>(key, (uint64_t)ps, bq, bo);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) blk[q] = philox(key, (uint64_t)ps, b0 + (uint64_t)q * (uint64_t)(P / 4));
-    const uint4 ex = philox(key, (uint64_t)ps, be);
+    for (int q = 0; q < 4; ++q) blk[q] = bo[q];
+    const uint4 ex = bo[4];
     if (lane < 4) S.xch[warp * 5 + lane] = ex;
     if (warp == nw - 1 && lane == 3) {
       const uint4 y = off == 3 ? philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P + 1) : ex;
@@ -1009,9 +1014,12 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           mj = fmaxf(mj, __double2float_ru(ll));
         }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mj = fmaxf(mj, __shfl_xor_sync(0xffffffffu, mj, o));
-      if (lane == 0) mb[j * 32 + warp] = mj;
+      // warp max through an order-preserving int key (one REDUX instead of 5 shuffles)
+      int key = __float_as_int(mj);
+      key ^= (key >> 31) & 0x7fffffff;
+      key = __reduce_max_sync(0xffffffffu, key);
+      key ^= (key >> 31) & 0x7fffffff;
+      if (lane == 0) mb[j * 32 + warp] = __int_as_float(key);
     }
     __syncthreads();
     double shift = 0.0;  // sum_j s'_j, in stage order
