@@ -207,14 +207,11 @@ struct ut_vecenv {
   int np = 1024;              // particle capacity of the step kernel instance
   size_t smem_reset = 0;      // the reset kernel always uses the 1024 layout
 
-  int ppt = kPPT;              // particles per thread of the step kernel (2: 512-thread CTAs)
   int nt_reset = 0;
 
   int launch_step(int mode) {
     const dim3 g((unsigned)grid), b((unsigned)nt);
-    if (full && np == 1024 && ppt == 2)
-      step_kernel<2, 1024, true><<<g, b, smem, stream>>>(B, mode, d_status);
-    else if (full && np == 1024)
+    if (full && np == 1024)
       step_kernel<kPPT, 1024, true><<<g, b, smem, stream>>>(B, mode, d_status);
     else if (full && np == 512)
       step_kernel<kPPT, 512, true><<<g, b, smem, stream>>>(B, mode, d_status);
@@ -351,13 +348,7 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   v->full = (v->P == v->nt * kPPT) && (v->P == 1024 || v->P == 512 || v->P == 256);
   v->np = v->full ? v->P : 1024;
   const void* fn = nullptr;
-  const char* ppt_env = getenv("UT_DEBUG_PPT");
-  if (v->full && v->P == 1024 && ppt_env && atoi(ppt_env) == 2) {
-    v->ppt = 2;
-    v->nt = 512;
-    fn = (const void*)step_kernel<2, 1024, true>;
-    v->smem = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
-  } else if (v->np == 1024 && v->full) {
+  if (v->np == 1024 && v->full) {
     fn = (const void*)step_kernel<kPPT, 1024, true>;
     v->smem = smem_bytes<1024>(v->A_max, v->T_max, v->nt);
   } else if (v->np == 512) {

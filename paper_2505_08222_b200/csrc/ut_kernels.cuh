@@ -72,11 +72,6 @@ struct Smem {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline size_t resample_bytes(int P) {
-  const size_t a = sizeof(double) * 5 * (size_t)P;   // cum + 4 staged fields
-  const size_t b = (size_t)4 * (8 * (size_t)P + 8);  // re-init words
-  return align16(a > b ? a : b);
-}
 
 // Fixed-size part of the layout for a particle capacity NP (compile-time
 // offsets: every access is an LDS/STS with an immediate offset). The
@@ -90,8 +85,10 @@ struct FixedSmem {
   double bc[16];
   uint4 xch[32 * 5];
   uint64_t mbar[2];
+  // one particle set: the TMA landing zone of the set being read, then (once
+  // every thread holds its particles) the staging of the exact update and the
+  // resample, and in the reset phase the re-init words
   double pf[5 * NP];
-  double area[(5 * NP > 4 * NP + 4 ? 5 * NP : 4 * NP + 4)];  // resample cum + staging | re-init words
   DevConfig cfg;
 };
 
@@ -119,8 +116,8 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int sA, int sT) {
   S.xch = F.xch;
   S.mbar = F.mbar;
   S.pf = F.pf;
-  S.cum = F.area;
-  S.st = F.area + NP;
+  S.st = F.pf;
+  S.cum = F.pf + 4 * NP;
   size_t o = align16(sizeof(FixedSmem<NP>));
   S.meas = (double*)(base + o);
   o += align16(sizeof(double) * kMeasStride * sA * sT);
@@ -766,7 +763,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
       s.w[q] = inv_n;
     }
   }
-  // S.st / S.cum are next written after this set's estimate barrier
+  // the set buffer is next written by the prefetch after this set's estimate barrier
 }
 
 // Issue the TMA prefetch of particle set g (5 fields x P doubles) into S.pf.
@@ -786,7 +783,7 @@ __device__ __forceinline__ void prefetch_set(const DevBatch& B, const Smem& S, i
 // finalize (env.cpp:397-409) for set (a, t) of env e (global set index gset).
 // FULL (P == blockDim * PPT, P % 4 == 0): the set arrives in S.pf by TMA
 // (phase `tphase`), the Philox blocks are computed in registers and the next
-// set `next` (>= 0) is prefetched once every thread has read this one.
+// set `next` (>= 0) is prefetched into S.pf after this set's last barrier.
 template <int PPT, bool FULL, int NW>
 __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, const Rec& rec,
                          int64_t gi, int64_t gset, int a, int t, uint32_t& tphase, int64_t next) {
@@ -831,31 +828,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // another) and hand them over through the warp's xch slots. The last warp's
   // segment-3 extra block, pos/4 + P, also holds the resample draw at pos + 4P.
   uint4 blk[4];
-  if (FULL && noise && PPT == 2) {
-    // PPT = 2 (512 threads): a warp's 64 particles use blocks [16w, 16w + 16] of
-    // each segment. Lane pair (2m, 2m+1) computes block 16w + m of segments
-    // {0, 1} / {2, 3}, lanes 0..3 block 16w + 16 of segment lane as a third
-    // chain; all 68 land in the warp's staging slots (the resample area, free
-    // until this set's update) in segment-major word order, so particle k's word
-    // for segment q sits at word q*68 + off + (k - 64w).
-    uint4* stg = reinterpret_cast<uint4*>(S.st) + warp * 68;
-    const uint64_t wb = (pos >> 2) + (uint64_t)(16 * warp);
-    const int m = lane >> 1, qa = (lane & 1) * 2;
-    const uint4 b0 = philox(key, (uint64_t)ps, wb + (uint64_t)qa * (uint64_t)(P / 4) + (uint64_t)m);
-    const uint4 b1 = philox(key, (uint64_t)ps, wb + (uint64_t)(qa + 1) * (uint64_t)(P / 4) + (uint64_t)m);
-    const uint4 ex = philox(key, (uint64_t)ps, wb + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + 16u);
-    stg[qa * 17 + m] = b0;
-    stg[(qa + 1) * 17 + m] = b1;
-    if (lane < 4) stg[lane * 17 + 16] = ex;
-    if (warp == nw - 1 && lane == 3) {
-      const uint4 y = off == 3 ? philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P + 1) : ex;
-      uint32_t w2[4];
-      words_at(ex, y, off, w2);
-      reinterpret_cast<uint32_t*>(S.bc)[0] = w2[0];
-      reinterpret_cast<uint32_t*>(S.bc)[1] = w2[1];
-    }
-    __syncwarp();
-  } else if (FULL && noise) {
+  if (FULL && noise) {
     const uint64_t b0 = (pos >> 2) + (uint64_t)tid;
     const uint64_t bq[5] = {b0, b0 + (uint64_t)(P / 4), b0 + 2 * (uint64_t)(P / 4), b0 + 3 * (uint64_t)(P / 4),
                             (pos >> 2) + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + (uint64_t)(32 * (warp + 1))};
@@ -889,13 +862,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   float zpx[PPT], zpy[PPT], zvx[PPT], zvy[PPT];  // out[k], out[P+k], out[2P+k], out[3P+k]
   if (noise) {
     uint32_t W[4][PPT];  // [segment][particle]
-    if (FULL && PPT == 2) {
-      const uint32_t* sw = reinterpret_cast<const uint32_t*>(S.st) + warp * 68 * 4 + off + 2 * lane;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int j = 0; j < PPT; ++j) W[q][j] = sw[q * 68 + j];
-    } else if (FULL) {
+    if (FULL) {
       if constexpr (PPT == 4) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -950,8 +917,6 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       s.vx[q] = u.x, s.vx[q + 1] = u.y, s.vy[q] = v.x, s.vy[q + 1] = v.y;
       s.w[q] = w.x, s.w[q + 1] = w.y;
     }
-    __syncthreads();  // S.pf consumed
-    if (tid == 0 && next >= 0) prefetch_set(B, S, next, P);
   }
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
@@ -1069,6 +1034,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     if (exact && tid == 0) STAT(9) += 1.0;
   }
   if (exact && nm > 0) {
+    __syncthreads();  // every thread holds its particles: S.pf becomes the staging area
 #pragma unroll
     for (int q = 0; q < PPT; ++q)
       if (FULL || k0 + q < P) {
@@ -1114,7 +1080,12 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
            (unsigned long long)pos);
 
   // ---- estimate (env.cpp:403-407)
+  // The set buffer is free once every thread is past the estimate barrier: the
+  // next set of this chunk is prefetched into it then (generic-proxy writes to
+  // it are fenced against the async-proxy copy first).
+  if (FULL) fence_proxy_async();
   const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R);
+  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
   if (FULL) {
 #pragma unroll
     for (int q = 0; q < PPT; q += 2) {
@@ -1198,7 +1169,7 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
   const int k0 = tid * PPT;
   uint64_t pos = (uint64_t)TRK(K_POS, ti);
   const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)ps);
-  uint32_t* words = reinterpret_cast<uint32_t*>(S.cum);  // the resample area
+  uint32_t* words = reinterpret_cast<uint32_t*>(S.pf);  // the set buffer (no prefetch in flight here)
   __syncthreads();  // that area may still be read by the previous phase
   gen_words(words, key, (uint64_t)ps, pos, 8ull * (uint64_t)P);
   __syncthreads();
@@ -1285,8 +1256,7 @@ __device__ __noinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t
 
 // The fused step.
 template <int PPT, int NP, bool FULL>
-__global__ void __launch_bounds__(PPT == 2 ? 512 : 256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode,
-                                                                                       int32_t* status) {
+__global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem S = carve<NP>(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT);
   const DevBatch& Bg = *B.self;  // cold paths read the global copy
@@ -1298,10 +1268,13 @@ __global__ void __launch_bounds__(PPT == 2 ? 512 : 256, UT_STEP_MIN_BLOCKS) step
   const int64_t set_end = hi < B.n_envs ? set_off(B, hi) : set_off(B, hi - 1) + cfg_of(B, hi - 1).A * cfg_of(B, hi - 1).T;
   __syncthreads();
   uint32_t tphase = 0;
-  if (FULL && threadIdx.x == 0 && lo < hi) prefetch_set(B, S, set_off(B, lo), B.P);
   long long cyc[kPhaseCount] = {0, 0, 0, 0};
   for (int64_t e0 = lo; e0 < hi; e0 += blockDim.x) {
     const int64_t e1 = min(hi, e0 + (int64_t)blockDim.x);
+    // the chunk's sets [set_off(e0), chunk_end) are prefetched one ahead; the
+    // set buffer is free at chunk boundaries (the reset phase uses it)
+    const int64_t chunk_end = e1 < B.n_envs ? set_off(B, e1) : set_end;
+    if (FULL && threadIdx.x == 0) prefetch_set(B, S, set_off(B, e0), B.P);
     long long t0 = clock64();
     // ---- 1. prologue, one env per thread
     {
@@ -1324,7 +1297,7 @@ __global__ void __launch_bounds__(PPT == 2 ? 512 : 256, UT_STEP_MIN_BLOCKS) step
         for (int t = 0; t < nT; ++t) {
           const int64_t g = so + a * nT + t;
           step_set<PPT, FULL, FULL ? NP / (32 * PPT) : 0>(c, B, S, R, rec, gi, g, a, t, tphase,
-                                                           g + 1 < set_end ? g + 1 : -1);
+                                                           g + 1 < chunk_end ? g + 1 : -1);
         }
       __syncthreads();  // S.cfg / meas / mlist reused by the next env
     }
@@ -1357,6 +1330,7 @@ __global__ void __launch_bounds__(PPT == 2 ? 512 : 256, UT_STEP_MIN_BLOCKS) step
       write_outputs(Bg, e0, e1, S.flags, kChunkFlagSpawned, false);
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagSpawned)) B.step[e] = 0;
     }
+    if (FULL) fence_proxy_async();  // re-init words in the set buffer vs the next chunk's prefetch
     __syncthreads();
     cyc[PH_RESET] += clock64() - t3;
   }
