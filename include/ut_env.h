@@ -198,6 +198,14 @@ int ut_vecenv_phase_cycles(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset);
  * required length; UT_ERR_DATA if `cap` is too small / the blob is malformed. */
 int ut_env_serialize(ut_vecenv* v, int64_t env, double* blob, size_t cap, size_t* len);
 int ut_env_deserialize(ut_vecenv* v, int64_t env, const double* blob, size_t len);
+/* Batched serialize_state / deserialize_state of envs [env_begin, env_end) (the
+ * checkpoint path, marl.cpp:741-805): the blobs back to back, env e's at the sum
+ * of the blob lengths before it; packed / unpacked on the device straight from the
+ * state store. export: `len` receives the total (blobs may be NULL to query),
+ * UT_ERR_DATA if `cap` is too small. import: UT_ERR_DATA unless len is exact. */
+int ut_vecenv_export_state(ut_vecenv* v, int64_t env_begin, int64_t env_end, double* blobs, size_t cap,
+                           size_t* len);
+int ut_vecenv_import_state(ut_vecenv* v, int64_t env_begin, int64_t env_end, const double* blobs, size_t len);
 /* world().step (env.hpp:50), read by Trainer::collect_rollout (marl.cpp:211,227). */
 int ut_env_world_step(ut_vecenv* v, int64_t env, int32_t* step);
 

@@ -141,6 +141,19 @@ class VecEnv {
     dirty_ = true;
   }
 
+  // batched serialize / deserialize of envs [begin, end), blobs back to back (checkpoints)
+  std::vector<double> export_state(int64_t begin, int64_t end) const {
+    size_t len = 0;
+    check(ut_vecenv_export_state(h_, begin, end, nullptr, 0, &len));
+    std::vector<double> blobs(len);
+    check(ut_vecenv_export_state(h_, begin, end, blobs.data(), blobs.size(), &len));
+    return blobs;
+  }
+  void import_state(int64_t begin, int64_t end, const std::vector<double>& blobs) {
+    check(ut_vecenv_import_state(h_, begin, end, blobs.data(), blobs.size()));
+    dirty_ = true;
+  }
+
   const ut_buffers& device_buffers() const { return buf_; }
   ut_vecenv* handle() const { return h_; }
 

@@ -111,6 +111,9 @@ def declare_product(lib):
                                        C.POINTER(C.c_size_t)]),
         "ut_env_deserialize": (C.c_int, [P, I64, C.POINTER(C.c_double), C.c_size_t]),
         "ut_env_world_step": (C.c_int, [P, I64, C.POINTER(I32)]),
+        "ut_vecenv_export_state": (C.c_int, [P, I64, I64, C.POINTER(C.c_double), C.c_size_t,
+                                             C.POINTER(C.c_size_t)]),
+        "ut_vecenv_import_state": (C.c_int, [P, I64, I64, C.POINTER(C.c_double), C.c_size_t]),
         "ut_benchmark_sps": (C.c_int, [cfgp, I64, I32, C.c_int, U64, I32, C.c_int,
                                        C.POINTER(BenchmarkReport)]),
         "ut_vecenv_enable_phase_timing": (C.c_int, [P, C.c_int]),
@@ -148,6 +151,7 @@ PRODUCT_SYMBOLS = (
     "ut_vecenv_refresh_outputs", "ut_vecenv_buffers", "ut_vecenv_copy_outputs",
     "ut_vecenv_set_stream", "ut_vecenv_synchronize", "ut_vecenv_stats", "ut_vecenv_launch_count",
     "ut_env_serialize", "ut_env_deserialize", "ut_env_world_step", "ut_benchmark_sps",
+    "ut_vecenv_export_state", "ut_vecenv_import_state",
     "ut_vecenv_enable_phase_timing", "ut_vecenv_phase_cycles",
     "ut_last_error", "ut_abi_version",
 )

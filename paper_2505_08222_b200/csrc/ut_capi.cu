@@ -15,6 +15,7 @@
 
 #include "ut_env.h"
 #include "ut_kernels.cuh"
+#include "ut_blob.cuh"
 
 using namespace ut;
 
@@ -760,6 +761,111 @@ int ut_env_deserialize(ut_vecenv* v, int64_t e, const double* blob, size_t len) 
   for (int k = 0; k < 5; ++k)
     UT_CUDA(cudaMemcpy(dst[k] + (size_t)v->set_at(e) * P, f[k].data(), sizeof(double) * nset, cudaMemcpyHostToDevice));
   return UT_OK;
+}
+
+// Batched serialize / deserialize of envs [e_begin, e_end): blobs back to back
+// (env e's at the sum of the lengths before it), packed on the device one CTA
+// per env and moved in staging batches of <= kBlobStaging bytes.
+namespace {
+constexpr size_t kBlobStaging = size_t(256) << 20;
+
+int blob_batches(ut_vecenv* v, int64_t e_begin, int64_t e_end, bool do_export, double* host_out,
+                 const double* host_in) {
+  int sms = 0;
+  UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, v->device));
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  std::vector<int64_t> off;
+  size_t host_pos = 0;
+  double* stage = nullptr;
+  int64_t* d_off = nullptr;
+  size_t stage_cap = 0, off_cap = 0;
+  int rc = UT_OK;
+  for (int64_t b = e_begin; b < e_end && rc == UT_OK;) {
+    off.assign(1, 0);
+    int64_t e = b;
+    while (e < e_end) {
+      const DevConfig& d = v->cfg(e);
+      const int64_t l = blob_len(d.A, d.T, d.P);
+      if (e > b && (size_t)(off.back() + l) * sizeof(double) > kBlobStaging) break;
+      off.push_back(off.back() + l);
+      ++e;
+    }
+    const int64_t n = e - b;
+    const size_t words = (size_t)off.back();
+    if (words > stage_cap) {
+      cudaFree(stage);
+      stage = nullptr;
+      if (cudaMalloc(&stage, words * sizeof(double)) != cudaSuccess) {
+        rc = fail(UT_ERR_RUNTIME, "state export/import: cannot allocate %zu bytes of staging", words * 8);
+        break;
+      }
+      stage_cap = words;
+    }
+    if ((size_t)n + 1 > off_cap) {
+      cudaFree(d_off);
+      d_off = nullptr;
+      if (cudaMalloc(&d_off, (n + 1) * sizeof(int64_t)) != cudaSuccess) {
+        rc = fail(UT_ERR_RUNTIME, "state export/import: cannot allocate offsets");
+        break;
+      }
+      off_cap = (size_t)n + 1;
+    }
+    cudaError_t err = cudaMemcpyAsync(d_off, off.data(), (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, v->stream);
+    const unsigned grid = (unsigned)std::min<int64_t>(n, (int64_t)sms * 8);
+    if (err == cudaSuccess && do_export) {
+      pack_blobs_kernel<<<grid, 256, 0, v->stream>>>(v->B, b, n, d_off, stage);
+      err = cudaGetLastError();
+      if (err == cudaSuccess)
+        err = cudaMemcpyAsync(host_out + host_pos, stage, words * sizeof(double), cudaMemcpyDeviceToHost, v->stream);
+    } else if (err == cudaSuccess) {
+      err = cudaMemcpyAsync(stage, host_in + host_pos, words * sizeof(double), cudaMemcpyHostToDevice, v->stream);
+      if (err == cudaSuccess) {
+        unpack_blobs_kernel<<<grid, 256, 0, v->stream>>>(v->B, b, n, d_off, stage);
+        err = cudaGetLastError();
+      }
+    }
+    v->launches += 1;
+    if (err == cudaSuccess) err = cudaStreamSynchronize(v->stream);
+    if (err != cudaSuccess) rc = fail(UT_ERR_RUNTIME, "state export/import: %s", cudaGetErrorString(err));
+    host_pos += words;
+    b = e;
+  }
+  cudaFree(stage);
+  cudaFree(d_off);
+  return rc;
+}
+
+int blob_range(ut_vecenv* v, int64_t e_begin, int64_t e_end, size_t* total, const char* what) {
+  if (e_begin < 0 || e_end > v->n_envs || e_begin > e_end)
+    return fail(UT_ERR_CONTRACT, "%s: env range [%lld, %lld) outside [0, %lld)", what, (long long)e_begin,
+                (long long)e_end, (long long)v->n_envs);
+  size_t t = 0;
+  for (int64_t e = e_begin; e < e_end; ++e) {
+    const DevConfig& d = v->cfg(e);
+    t += (size_t)blob_len(d.A, d.T, d.P);
+  }
+  *total = t;
+  return UT_OK;
+}
+}  // namespace
+
+int ut_vecenv_export_state(ut_vecenv* v, int64_t e_begin, int64_t e_end, double* blobs, size_t cap, size_t* len) {
+  size_t total = 0;
+  int rc = blob_range(v, e_begin, e_end, &total, "export_state");
+  if (rc) return rc;
+  *len = total;
+  if (!blobs) return UT_OK;
+  if (cap < total) return fail(UT_ERR_DATA, "export_state: buffer of %zu doubles too small (need %zu)", cap, total);
+  return blob_batches(v, e_begin, e_end, true, blobs, nullptr);
+}
+
+int ut_vecenv_import_state(ut_vecenv* v, int64_t e_begin, int64_t e_end, const double* blobs, size_t len) {
+  size_t total = 0;
+  int rc = blob_range(v, e_begin, e_end, &total, "import_state");
+  if (rc) return rc;
+  if (len < total) return fail(UT_ERR_DATA, "environment state blobs truncated");
+  if (len > total) return fail(UT_ERR_DATA, "environment state blobs have trailing data");
+  return blob_batches(v, e_begin, e_end, false, nullptr, blobs);
 }
 
 int ut_env_world_step(ut_vecenv* v, int64_t e, int32_t* step) {

@@ -323,6 +323,26 @@ class VecEnv:
         b = np.ascontiguousarray(blob, np.float64)
         _check(self._lib.ut_env_deserialize(self._h, env, b.ctypes.data_as(C.POINTER(C.c_double)), b.size))
 
+    def export_state(self, begin: int = 0, end: Optional[int] = None) -> np.ndarray:
+        """serialize_state of envs [begin, end) in one device pass: the blobs back
+        to back (shape (n, blob_len) for a homogeneous fleet, flat otherwise)."""
+        end = self.n_envs() if end is None else end
+        n = C.c_size_t()
+        _check(self._lib.ut_vecenv_export_state(self._h, begin, end, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.float64)
+        _check(self._lib.ut_vecenv_export_state(self._h, begin, end, out.ctypes.data_as(C.POINTER(C.c_double)),
+                                                n.value, C.byref(n)))
+        if len(self._cfgs) == 1 and end > begin:
+            out = out.reshape(end - begin, -1)
+        return out
+
+    def import_state(self, blobs, begin: int = 0, end: Optional[int] = None):
+        """deserialize_state of envs [begin, end) from blobs back to back."""
+        end = self.n_envs() if end is None else end
+        b = np.ascontiguousarray(blobs, np.float64).reshape(-1)
+        _check(self._lib.ut_vecenv_import_state(self._h, begin, end, b.ctypes.data_as(C.POINTER(C.c_double)),
+                                                b.size))
+
     def world_step(self, env: int) -> int:
         s = C.c_int32()
         _check(self._lib.ut_env_world_step(self._h, env, C.byref(s)))

@@ -23,8 +23,11 @@ int main() {
     for (double r : venv.rewards()) rsum += r;
     int done = 0;
     for (auto d : venv.dones()) done += d;
-    std::printf("{\"ok\": 1, \"reward_sum\": %.17g, \"dones\": %d, \"obs00\": %.17g, \"step0\": %d, \"blob\": %zu}\n",
-                rsum, done, venv.obs_stack()(0, 0), venv.world_step(0), venv.serialize_state(0).size());
+    const std::vector<double> all = venv.export_state(0, venv.n_envs());
+    venv.import_state(0, venv.n_envs(), all);
+    std::printf("{\"ok\": 1, \"reward_sum\": %.17g, \"dones\": %d, \"obs00\": %.17g, \"step0\": %d, \"blob\": %zu, "
+                "\"all\": %zu}\n",
+                rsum, done, venv.obs_stack()(0, 0), venv.world_step(0), venv.serialize_state(0).size(), all.size());
   } catch (const ut::DeviceError& e) {
     std::printf("{\"ok\": 0, \"error\": \"DeviceError\"}\n");
   } catch (const std::exception& e) {

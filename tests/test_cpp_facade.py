@@ -50,3 +50,4 @@ def test_facade_matches_python_mirror(tmp_path, cuda_device):
     assert d["obs00"] == float(h["obs"][0, 0])
     assert d["step0"] == v.world_step(0)
     assert d["blob"] == v.serialize_state(0).size
+    assert d["all"] == 4 * d["blob"]
