@@ -61,8 +61,8 @@ def algorithmic_bytes_per_env_step(A, T, P, rec_words):
 
 def rec_words_for(A, T):
     """Words of one env record (csrc/ut_layout.h layout_config)."""
-    o_track = 8 + 6 * A + 8 * T + T + 6 * A * A
-    return o_track + 10 * A * T + 10
+    o_track = 11 + 6 * A + 8 * T + T + 6 * A * A
+    return o_track + 10 * A * T + 16
 
 
 class ClockSampler:

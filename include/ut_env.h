@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define UT_ABI_VERSION 1
+#define UT_ABI_VERSION 2
 
 enum ut_status {
   UT_OK = 0,
@@ -124,6 +124,15 @@ enum {
   UT_STAT_PF_UPDATES,         /* particle-filter measurement updates      */
   UT_STAT_PF_RESAMPLES,       /* particle-filter resamples                */
   UT_STAT_PF_EXACT_PATH,      /* sets that took the exact sequential update path */
+  /* curriculum::evaluate's Table-2 metrics (curriculum.cpp:267-356) over the
+   * completed episodes: per-episode mean agent-target distance and mean tracking
+   * error (sums and sums of squares), episodes with a collision / a lost target */
+  UT_STAT_EVAL_DIST_SUM,
+  UT_STAT_EVAL_DIST_SQ,
+  UT_STAT_EVAL_ERR_SUM,
+  UT_STAT_EVAL_ERR_SQ,
+  UT_STAT_EVAL_COLLIDED_EPISODES,
+  UT_STAT_EVAL_LOST_EPISODES,
   UT_N_STATS
 };
 

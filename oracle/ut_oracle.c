@@ -343,6 +343,8 @@ typedef struct {
   double *err, *dist;
   uint8_t* lost;
   double episode_return; /* stats only */
+  double ev_dist, ev_err; /* evaluation accumulators (curriculum.cpp:286-325) */
+  int ev_flags;
 } uto_env;
 
 struct uto_vecenv {
@@ -695,6 +697,9 @@ static int spawn(uto_vecenv* v, int64_t e) {
   E->done = 0;
   E->collision = 0;
   E->episode_return = 0.0;
+  E->ev_dist = 0.0;
+  E->ev_err = 0.0;
+  E->ev_flags = 0;
   return UT_OK;
 }
 
@@ -888,9 +893,33 @@ static int env_step(uto_vecenv* v, int64_t e, const int32_t* actions) {
   v->stats[UT_STAT_COLLISION_STEPS] += E->collision;
   for (int t = 0; t < v->T; ++t) v->stats[UT_STAT_LOST_TARGET_STEPS] += E->lost[t];
   E->episode_return += E->reward;
+  /* curriculum::evaluate's per-episode accumulation (curriculum.cpp:307-325) */
+  {
+    int lost_any = 0;
+    for (int t = 0; t < v->T; ++t) {
+      E->ev_err += E->err[t];
+      lost_any |= E->lost[t];
+    }
+    for (int a = 0; a < v->A; ++a)
+      for (int t = 0; t < v->T; ++t)
+        E->ev_dist += hypot(E->agents[a].x - E->targets[t].x, E->agents[a].y - E->targets[t].y);
+    E->ev_flags |= (E->collision ? 1 : 0) | (lost_any ? 2 : 0);
+  }
   if (E->done) {
     v->stats[UT_STAT_EPISODES_DONE] += 1.0;
     v->stats[UT_STAT_EPISODE_RETURN_SUM] += E->episode_return;
+    {
+      const double md = E->ev_dist / ((double)v->cfg.horizon * v->A * v->T);
+      const double me = E->ev_err / ((double)v->cfg.horizon * v->T);
+      v->stats[UT_STAT_EVAL_DIST_SUM] += md;
+      v->stats[UT_STAT_EVAL_DIST_SQ] += md * md;
+      v->stats[UT_STAT_EVAL_ERR_SUM] += me;
+      v->stats[UT_STAT_EVAL_ERR_SQ] += me * me;
+      v->stats[UT_STAT_EVAL_COLLIDED_EPISODES] += (E->ev_flags & 1) ? 1.0 : 0.0;
+      v->stats[UT_STAT_EVAL_LOST_EPISODES] += (E->ev_flags & 2) ? 1.0 : 0.0;
+      E->ev_dist = E->ev_err = 0.0;
+      E->ev_flags = 0;
+    }
     for (int a = 0; a < v->A; ++a) build_observation(v, e, a, v->final_obs);
     const double rew = E->reward;
     const uint8_t col = E->collision;
@@ -1090,6 +1119,14 @@ int uto_copy_outputs(uto_vecenv* v, const ut_host_outputs* d) {
     if (d->collision) d->collision[e] = E->collision;
     if (d->step) d->step[e] = E->step;
   }
+  return UT_OK;
+}
+
+int uto_eval_acc(uto_vecenv* v, int64_t e, double out[3]) {
+  if (e < 0 || e >= v->n) return set_err(UT_ERR_CONTRACT, "eval_acc: env out of range");
+  out[0] = v->envs[e].ev_dist;
+  out[1] = v->envs[e].ev_err;
+  out[2] = (double)v->envs[e].ev_flags;
   return UT_OK;
 }
 

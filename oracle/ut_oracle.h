@@ -32,6 +32,9 @@ int uto_copy_outputs(uto_vecenv* v, const ut_host_outputs* dst);
 int uto_serialize(uto_vecenv* v, int64_t env, double* blob, size_t cap, size_t* len);
 int uto_deserialize(uto_vecenv* v, int64_t env, const double* blob, size_t len);
 int uto_stats(uto_vecenv* v, double out[UT_N_STATS]);
+/* the running episode's evaluation accumulators of env e: sum of agent-target
+ * distances, sum of tracking errors, collided | lost<<1 (test hook) */
+int uto_eval_acc(uto_vecenv* v, int64_t e, double out[3]);
 const char* uto_last_error(void);
 
 /* primitives exposed for unit tests */

@@ -15,7 +15,10 @@ UT_HEADING_DEFAULT, UT_HEADING_BUCKET = 0, 1
 STAT_NAMES = (
     "env_steps", "reward_sum", "track_err_sum", "episodes_done", "episode_return_sum",
     "collision_steps", "lost_target_steps", "pf_updates", "pf_resamples", "pf_exact_path",
+    "eval_dist_sum", "eval_dist_sq", "eval_err_sum", "eval_err_sq", "eval_collided_episodes",
+    "eval_lost_episodes",
 )
+UT_ABI_VERSION = 2
 UT_N_STATS = len(STAT_NAMES)
 
 

@@ -26,7 +26,7 @@ def lib():
                 "(or __graft_entry__.build()); there is no CPU fallback")
         handle = C.CDLL(str(LIB_PATH))
         _abi.declare_product(handle)
-        if handle.ut_abi_version() != 1:
+        if handle.ut_abi_version() != _abi.UT_ABI_VERSION:
             raise NativeLibraryMissing("libutrack_b200.so ABI version mismatch")
         _lib = handle
     return _lib

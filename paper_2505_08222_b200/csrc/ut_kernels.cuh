@@ -304,7 +304,7 @@ __device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B,
 __device__ __noinline__ bool env_epilogue(const DevConfig& c, const DevBatch& B, int64_t e) {
   const Rec rec = rec_of(B, e);
   const int A = c.A, T = c.T, Tm = B.T_max;
-  double reward_sum = 0.0, follow_sum = 0.0, err_sum = 0.0, lost_n = 0.0;
+  double reward_sum = 0.0, follow_sum = 0.0, err_sum = 0.0, lost_n = 0.0, dist_all = 0.0;
   for (int t = 0; t < T; ++t) {
     const double tx = TG(V_X, t), ty = TG(V_Y, t);
     double best_err = CUDART_INF, best_dist = CUDART_INF;
@@ -316,6 +316,7 @@ __device__ __noinline__ bool env_epilogue(const DevConfig& c, const DevBatch& B,
     for (int a = 0; a < A; ++a) {
       const double d = hypot(AG(V_X, a) - tx, AG(V_Y, a) - ty);
       best_dist = d < best_dist ? d : best_dist;
+      dist_all = dist_all + d;
     }
     const bool lost = rec[c.o_miss + t] >= (double)c.lost_steps;
     B.track_err[e * Tm + t] = best_err;
@@ -366,9 +367,27 @@ __device__ __noinline__ bool env_epilogue(const DevConfig& c, const DevBatch& B,
   STAT(5) += crash ? 1.0 : 0.0;
   STAT(6) += lost_n;
   rec[R_EP_RETURN] += reward;
+  // evaluation accumulators (curriculum.cpp:307-325, agents outer over targets
+  // there; here targets outer -- a different summation order of the same terms)
+  rec[R_EV_DIST] += dist_all;
+  rec[R_EV_ERR] += err_sum;
+  rec[R_EV_FLAGS] = (double)((int)rec[R_EV_FLAGS] | (crash ? 1 : 0) | (lost_n > 0.0 ? 2 : 0));
   if (done) {
     STAT(3) += 1.0;
     STAT(4) += rec[R_EP_RETURN];
+    // per-episode means over the horizon's steps (curriculum.cpp:327-328)
+    const double md = rec[R_EV_DIST] / ((double)c.horizon * A * T);
+    const double me = rec[R_EV_ERR] / ((double)c.horizon * T);
+    const int fl = (int)rec[R_EV_FLAGS];
+    STAT(10) += md;
+    STAT(11) += md * md;
+    STAT(12) += me;
+    STAT(13) += me * me;
+    STAT(14) += (fl & 1) ? 1.0 : 0.0;
+    STAT(15) += (fl & 2) ? 1.0 : 0.0;
+    rec[R_EV_DIST] = 0.0;
+    rec[R_EV_ERR] = 0.0;
+    rec[R_EV_FLAGS] = 0.0;
   }
   return done;
 }
@@ -430,6 +449,9 @@ __device__ __noinline__ bool spawn_serial(const DevConfig& c, const DevBatch& B,
   for (int t = 0; t < T; ++t) rec[c.o_miss + t] = 0.0;
   rec[R_STEP] = 0.0;
   rec[R_EP_RETURN] = 0.0;
+  rec[R_EV_DIST] = 0.0;
+  rec[R_EV_ERR] = 0.0;
+  rec[R_EV_FLAGS] = 0.0;
   rec[R_ENV_POS] = (double)rng.pos;
   rec[R_ENV_HAVE_SPARE] = rng.have_spare ? 1.0 : 0.0;
   rec[R_ENV_SPARE] = rng.spare;

@@ -29,7 +29,13 @@ enum : int {
   R_BENCH_POS = 5,
   R_EP_RETURN = 6,
   R_LAST_DONE = 7,
-  R_NSCALAR = 8
+  // evaluation accumulators of the running episode (curriculum.cpp:286-325):
+  // sum over steps of sum_{a,t} |agent - target|, of sum_t tracking error, and
+  // collided | lost<<1 -- not part of the state blob
+  R_EV_DIST = 8,
+  R_EV_ERR = 9,
+  R_EV_FLAGS = 10,
+  R_NSCALAR = 11
 };
 // vehicle fields (agents: first 6; targets: all 8)
 enum : int { V_X = 0, V_Y, V_Z, V_HEAD, V_SPEED, V_RUDDER, V_COUNTDOWN, V_CMD };
@@ -41,7 +47,7 @@ enum : int { K_EX = 0, K_EY, K_SPREAD, K_AGE, K_EVER, K_POS, K_HAVE_SPARE, K_SPA
              K_NFIELD };
 constexpr int K_NBLOB = 9;  // track fields carried by the state blob (env.cpp:578-583)
 
-constexpr int kStatCount = 10;  // ut_env.h UT_N_STATS
+constexpr int kStatCount = 16;  // ut_env.h UT_N_STATS
 
 // Resolved configuration for one fleet shape (EnvConfig after finalize()).
 struct DevConfig {

@@ -348,6 +348,26 @@ class VecEnv:
         _check(self._lib.ut_env_world_step(self._h, env, C.byref(s)))
         return s.value
 
+    def eval_metrics(self) -> dict:
+        """curriculum::evaluate's Table-2 metrics (curriculum.cpp:267-356) over the
+        episodes completed so far, accumulated on the device: mean / population std
+        of the per-episode mean agent-target distance and mean tracking error, and
+        the percentage of episodes with a collision / a lost target."""
+        st = dict(zip(_abi.STAT_NAMES, self.stats()))
+        n = st["episodes_done"]
+        if n <= 0:
+            return {"episodes": 0}
+
+        def mean_std(s, sq):
+            mu = s / n
+            return mu, float(np.sqrt(max(sq / n - mu * mu, 0.0)))
+
+        dm, ds = mean_std(st["eval_dist_sum"], st["eval_dist_sq"])
+        em, es = mean_std(st["eval_err_sum"], st["eval_err_sq"])
+        return {"episodes": int(n), "dist_mean": dm, "dist_std": ds, "err_mean": em, "err_std": es,
+                "collision_pct": 100.0 * st["eval_collided_episodes"] / n,
+                "loss_pct": 100.0 * st["eval_lost_episodes"] / n}
+
     def stats(self, reset: bool = False) -> np.ndarray:
         out = (C.c_double * _abi.UT_N_STATS)()
         _check(self._lib.ut_vecenv_stats(self._h, out, int(reset)))

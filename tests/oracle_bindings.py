@@ -59,6 +59,7 @@ def oracle_lib():
             getattr(lib, f).restype = C.c_float
         lib.uto_fill_normals.argtypes = [U64, U64, U64, I64, C.POINTER(C.c_float)]
         lib.uto_fill_normals.restype = None
+        lib.uto_eval_acc.argtypes = [P, I64, C.POINTER(C.c_double)]
         lib.uto_cr_grid.argtypes = [C.c_int, C.c_void_p]
         lib.uto_cr_grid.restype = None
         _oracle_lib = lib
@@ -197,6 +198,11 @@ class Oracle(_Base):
         out = (C.c_double * UT_N_STATS)()
         self._check(self.lib.uto_stats(self.h, out))
         return np.array(out[:])
+
+    def eval_acc(self, env):
+        out = (C.c_double * 3)()
+        self._check(self.lib.uto_eval_acc(self.h, env, out))
+        return tuple(out)
 
     def close(self):
         if getattr(self, "h", None):
