@@ -184,6 +184,16 @@ int ut_vecenv_refresh_outputs(ut_vecenv* v);
 
 int ut_vecenv_buffers(ut_vecenv* v, ut_buffers* out);
 int ut_vecenv_copy_outputs(ut_vecenv* v, const ut_host_outputs* dst);
+/* Output double buffering (n = 2; default 1): each step then writes the batch
+ * buffers the previous step did not, so the previous step's outputs can be
+ * copied out (ut_vecenv_copy_outputs_async) while the next step runs. The
+ * pointers of ut_vecenv_buffers() then change with every step (re-query after
+ * each); final_obs stays one buffer. Steps and resets wait for an asynchronous
+ * copy still reading the set they write. */
+int ut_vecenv_set_output_buffers(ut_vecenv* v, int n);
+/* Enqueues the D2H copies of the current outputs on `cuda_stream` after the
+ * handle's pending work, and returns; synchronize that stream before reading. */
+int ut_vecenv_copy_outputs_async(ut_vecenv* v, const ut_host_outputs* dst, void* cuda_stream);
 /* Runs subsequent work on a caller-owned cudaStream_t (NULL = the handle's own). */
 int ut_vecenv_set_stream(ut_vecenv* v, void* cuda_stream);
 int ut_vecenv_synchronize(ut_vecenv* v);

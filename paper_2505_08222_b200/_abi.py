@@ -107,6 +107,8 @@ def declare_product(lib):
         "ut_vecenv_buffers": (C.c_int, [P, C.POINTER(Buffers)]),
         "ut_vecenv_copy_outputs": (C.c_int, [P, C.POINTER(HostOutputs)]),
         "ut_vecenv_set_stream": (C.c_int, [P, P]),
+        "ut_vecenv_set_output_buffers": (C.c_int, [P, C.c_int]),
+        "ut_vecenv_copy_outputs_async": (C.c_int, [P, C.POINTER(HostOutputs), P]),
         "ut_vecenv_synchronize": (C.c_int, [P]),
         "ut_vecenv_stats": (C.c_int, [P, C.POINTER(C.c_double), C.c_int]),
         "ut_vecenv_launch_count": (I64, [P]),
@@ -154,7 +156,8 @@ PRODUCT_SYMBOLS = (
     "ut_vecenv_refresh_outputs", "ut_vecenv_buffers", "ut_vecenv_copy_outputs",
     "ut_vecenv_set_stream", "ut_vecenv_synchronize", "ut_vecenv_stats", "ut_vecenv_launch_count",
     "ut_env_serialize", "ut_env_deserialize", "ut_env_world_step", "ut_benchmark_sps",
-    "ut_vecenv_export_state", "ut_vecenv_import_state",
+    "ut_vecenv_export_state", "ut_vecenv_import_state", "ut_vecenv_set_output_buffers",
+    "ut_vecenv_copy_outputs_async",
     "ut_vecenv_enable_phase_timing", "ut_vecenv_phase_cycles",
     "ut_last_error", "ut_abi_version",
 )

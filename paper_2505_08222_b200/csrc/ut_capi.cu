@@ -143,6 +143,8 @@ struct ut_vecenv {
 
   ~ut_vecenv() {
     if (stream) cudaStreamSynchronize(stream);
+    for (cudaEvent_t ev : {copy_done[0], copy_done[1], step_done})
+      if (ev) cudaEventDestroy(ev);
     for (void* p : allocs) cudaFree(p);
     if (h_status) cudaFreeHost(h_status);
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -210,8 +212,43 @@ struct ut_vecenv {
 
   int nt_reset = 0;
 
+  // Output double buffering (ut_vecenv_set_output_buffers): every step writes the
+  // set the previous step did not, after any asynchronous copy still reading it
+  // (ut_vecenv_copy_outputs_async) has finished. final_obs is shared.
+  struct OutSet {
+    double *obs = nullptr, *global = nullptr, *rewards = nullptr, *track_err = nullptr, *min_dist = nullptr;
+    uint8_t *dones = nullptr, *masks = nullptr, *lost = nullptr, *collision = nullptr;
+    int32_t* step = nullptr;
+  };
+  OutSet out[2];
+  int n_out = 1, cur = 0;
+  cudaEvent_t copy_done[2] = {nullptr, nullptr};
+  cudaEvent_t step_done = nullptr;
+
+  void bind_outputs(int k) {
+    const OutSet& o = out[k];
+    B.obs = o.obs, B.global = o.global, B.rewards = o.rewards, B.track_err = o.track_err;
+    B.min_dist = o.min_dist, B.dones = o.dones, B.masks = o.masks, B.lost = o.lost;
+    B.collision = o.collision, B.step = o.step;
+  }
+  // before a kernel writes the output set k
+  int wait_outputs(int k) {
+    if (copy_done[k]) UT_CUDA(cudaStreamWaitEvent(stream, copy_done[k], 0));
+    return UT_OK;
+  }
+
   int launch_step(int mode) {
     const dim3 g((unsigned)grid), b((unsigned)nt);
+    int rc;
+    if (n_out == 2) {
+      const int t = cur ^ 1;
+      if ((rc = wait_outputs(t))) return rc;
+      bind_outputs(t);
+      cur = t;
+      if ((rc = sync_batch())) return rc;
+    } else if ((rc = wait_outputs(cur))) {
+      return rc;
+    }
     if (full && np == 1024)
       step_kernel<kPPT, 1024, true><<<g, b, smem, stream>>>(B, mode, d_status);
     else if (full && np == 512)
@@ -225,6 +262,8 @@ struct ut_vecenv {
     return UT_OK;
   }
   int launch_reset(int ctor) {
+    int rc;
+    if ((rc = wait_outputs(cur))) return rc;
     reset_kernel<kPPT, 1024><<<(unsigned)grid, nt_reset, smem_reset, stream>>>(B, ctor, d_status);
     ++launches;
     UT_CUDA(cudaGetLastError());
@@ -323,6 +362,7 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   if ((rc = v->alloc(&B.lost, (size_t)(n_envs * Tm)))) return rc;
   if ((rc = v->alloc(&B.collision, (size_t)n_envs))) return rc;
   if ((rc = v->alloc(&B.step, (size_t)n_envs))) return rc;
+  v->out[0] = {B.obs, B.global, B.rewards, B.track_err, B.min_dist, B.dones, B.masks, B.lost, B.collision, B.step};
   int32_t* acts;
   if ((rc = v->alloc(&acts, (size_t)(n_envs * Am)))) return rc;
   B.actions = acts;
@@ -535,12 +575,82 @@ int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps) {
 }
 
 int ut_vecenv_refresh_outputs(ut_vecenv* v) {
-  int sms = 0;
+  int sms = 0, rc;
   UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, v->device));
+  if ((rc = v->wait_outputs(v->cur))) return rc;
   tokens_kernel<<<(unsigned)(sms * 8), 256, 0, v->stream>>>(v->B);
   ++v->launches;
   UT_CUDA(cudaGetLastError());
   UT_CUDA(cudaStreamSynchronize(v->stream));
+  return UT_OK;
+}
+
+int ut_vecenv_set_output_buffers(ut_vecenv* v, int n) {
+  if (n != 1 && n != 2) return fail(UT_ERR_CONTRACT, "set_output_buffers: n must be 1 or 2");
+  if (n == v->n_out) return UT_OK;
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  for (cudaEvent_t ev : {v->copy_done[0], v->copy_done[1]})
+    if (ev) UT_CUDA(cudaEventSynchronize(ev));
+  if (n == 2 && !v->out[1].obs) {
+    const int64_t E = v->n_envs, Am = v->A_max, Tm = v->T_max;
+    ut_vecenv::OutSet& o = v->out[1];
+    int rc;
+    if ((rc = v->alloc(&o.obs, (size_t)(12 * v->B.obs_rows))) || (rc = v->alloc(&o.global, (size_t)(12 * v->B.global_rows))) ||
+        (rc = v->alloc(&o.rewards, (size_t)E)) || (rc = v->alloc(&o.dones, (size_t)E)) ||
+        (rc = v->alloc(&o.masks, (size_t)(E * Am * 5))) || (rc = v->alloc(&o.track_err, (size_t)(E * Tm))) ||
+        (rc = v->alloc(&o.min_dist, (size_t)(E * Tm))) || (rc = v->alloc(&o.lost, (size_t)(E * Tm))) ||
+        (rc = v->alloc(&o.collision, (size_t)E)) || (rc = v->alloc(&o.step, (size_t)E)))
+      return rc;
+  }
+  if (n == 1 && v->cur == 1) {  // keep the current outputs in set 0
+    const ut_vecenv::OutSet &a = v->out[0], &b = v->out[1];
+    const int64_t E = v->n_envs, Am = v->A_max, Tm = v->T_max;
+    auto cp = [&](void* d, const void* s2, size_t bytes) { return cudaMemcpyAsync(d, s2, bytes, cudaMemcpyDeviceToDevice, v->stream); };
+    UT_CUDA(cp(a.obs, b.obs, sizeof(double) * 12 * v->B.obs_rows));
+    UT_CUDA(cp(a.global, b.global, sizeof(double) * 12 * v->B.global_rows));
+    UT_CUDA(cp(a.rewards, b.rewards, sizeof(double) * E));
+    UT_CUDA(cp(a.dones, b.dones, (size_t)E));
+    UT_CUDA(cp(a.masks, b.masks, (size_t)(E * Am * 5)));
+    UT_CUDA(cp(a.track_err, b.track_err, sizeof(double) * E * Tm));
+    UT_CUDA(cp(a.min_dist, b.min_dist, sizeof(double) * E * Tm));
+    UT_CUDA(cp(a.lost, b.lost, (size_t)(E * Tm)));
+    UT_CUDA(cp(a.collision, b.collision, (size_t)E));
+    UT_CUDA(cp(a.step, b.step, sizeof(int32_t) * E));
+    v->cur = 0;
+    v->bind_outputs(0);
+    int rc;
+    if ((rc = v->sync_batch())) return rc;
+    UT_CUDA(cudaStreamSynchronize(v->stream));
+  }
+  v->n_out = n;
+  return UT_OK;
+}
+
+int ut_vecenv_copy_outputs_async(ut_vecenv* v, const ut_host_outputs* d, void* cuda_stream) {
+  cudaStream_t cs = static_cast<cudaStream_t>(cuda_stream);
+  if (!v->step_done) UT_CUDA(cudaEventCreateWithFlags(&v->step_done, cudaEventDisableTiming));
+  cudaEvent_t& done = v->copy_done[v->cur];
+  if (!done) UT_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  UT_CUDA(cudaEventRecord(v->step_done, v->stream));
+  UT_CUDA(cudaStreamWaitEvent(cs, v->step_done, 0));
+  const DevBatch& B = v->B;
+  const int64_t n = v->n_envs, Am = v->A_max, Tm = v->T_max;
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (!dst) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, cs);
+  };
+  UT_CUDA(cp(d->obs, B.obs, sizeof(double) * 12 * B.obs_rows));
+  UT_CUDA(cp(d->final_obs, B.final_obs, sizeof(double) * 12 * B.obs_rows));
+  UT_CUDA(cp(d->global_state, B.global, sizeof(double) * 12 * B.global_rows));
+  UT_CUDA(cp(d->rewards, B.rewards, sizeof(double) * n));
+  UT_CUDA(cp(d->dones, B.dones, (size_t)n));
+  UT_CUDA(cp(d->masks, B.masks, (size_t)(n * Am * 5)));
+  UT_CUDA(cp(d->tracking_error, B.track_err, sizeof(double) * n * Tm));
+  UT_CUDA(cp(d->min_agent_dist, B.min_dist, sizeof(double) * n * Tm));
+  UT_CUDA(cp(d->target_lost, B.lost, (size_t)(n * Tm)));
+  UT_CUDA(cp(d->collision, B.collision, (size_t)n));
+  UT_CUDA(cp(d->step, B.step, sizeof(int32_t) * n));
+  UT_CUDA(cudaEventRecord(done, cs));
   return UT_OK;
 }
 

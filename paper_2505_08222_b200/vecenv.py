@@ -185,6 +185,7 @@ class VecEnv:
         self._b = _abi.Buffers()
         _check(self._lib.ut_vecenv_buffers(self._h, C.byref(self._b)))
         self._views = {}
+        self._n_out = 1
 
     # -- shape (vecenv.hpp:29-33)
     def n_envs(self) -> int:
@@ -205,10 +206,27 @@ class VecEnv:
     def config(self):
         return self._config
 
+    # -- output buffering (ut_vecenv_set_output_buffers)
+    def set_output_buffers(self, n: int):
+        """n = 2: each step writes the batch buffers the previous step did not, so
+        copy_outputs_async() of one step overlaps the next step's kernel."""
+        _check(self._lib.ut_vecenv_set_output_buffers(self._h, n))
+        self._n_out = n
+        self._sync_buffers()
+
+    def _sync_buffers(self):
+        _check(self._lib.ut_vecenv_buffers(self._h, C.byref(self._b)))
+        self._views = {k: v for k, v in self._views.items() if k.startswith("pf_") or k == "final_obs"}
+
+    def _after_write(self):
+        if self._n_out == 2:
+            self._sync_buffers()
+
     # -- stepping
     def reset_all(self):
         """vecenv.cpp:69-77."""
         _check(self._lib.ut_vecenv_reset_all(self._h))
+        self._after_write()
 
     def step(self, actions):
         """vecenv.cpp:79-116. actions: n_envs x n_agents ints (numpy / list / CPU or
@@ -221,6 +239,7 @@ class VecEnv:
                     raise ContractViolation("vecenv step: wrong action count")
                 if t.is_cuda:
                     _check(self._lib.ut_vecenv_step(self._h, C.c_void_p(t.data_ptr()), 1))
+                    self._after_write()
                     return
                 actions = t.numpy()
         except ImportError:
@@ -229,12 +248,14 @@ class VecEnv:
         if a.size != self.n_envs() * self.n_agents():
             raise ContractViolation("vecenv step: wrong action count")
         _check(self._lib.ut_vecenv_step(self._h, C.c_void_p(a.ctypes.data), 0))
+        self._after_write()
 
     def step_policy(self, policy="random", n_steps: int = 1):
         """vecenv.cpp:118-143 (``n_steps`` > 1 runs back-to-back device steps)."""
         if policy not in _POLICIES:
             raise ContractViolation(f"unknown policy {policy!r}")
         _check(self._lib.ut_vecenv_step_policy(self._h, _POLICIES[policy], n_steps))
+        self._after_write()
 
     def refresh_outputs(self):
         """vecenv.cpp:145-150."""
@@ -309,6 +330,13 @@ class VecEnv:
         ho = _abi.HostOutputs(**{k: int(v.data_ptr() if hasattr(v, "data_ptr") else v.ctypes.data)
                                  for k, v in host.items()})
         _check(self._lib.ut_vecenv_copy_outputs(self._h, C.byref(ho)))
+
+    def copy_outputs_async(self, host: dict, stream_ptr: int):
+        """ut_vecenv_copy_outputs_async: enqueue the copies on a CUDA stream and
+        return (pinned host buffers; synchronize the stream before reading)."""
+        ho = _abi.HostOutputs(**{k: int(v.data_ptr() if hasattr(v, "data_ptr") else v.ctypes.data)
+                                 for k, v in host.items()})
+        _check(self._lib.ut_vecenv_copy_outputs_async(self._h, C.byref(ho), C.c_void_p(stream_ptr)))
 
     # -- per-env state (env.hpp:130-137)
     def serialize_state(self, env: int) -> np.ndarray:

@@ -327,3 +327,35 @@ def test_batched_state_export_mixed_fleet(cuda_device):
     assert flat.tobytes() == want.tobytes()
     gpu.import_state(flat)
     assert gpu.export_state().tobytes() == want.tobytes()
+
+
+def test_output_double_buffering_and_async_copies(cuda_device):
+    """set_output_buffers(2) + copy_outputs_async: every step's outputs arrive
+    intact while the next step writes the other buffer set."""
+    import torch
+    cfg, ora, gpu = make_pair(CONFIGS["c2_2v2"], 6, 31)
+    gpu.set_output_buffers(2)
+    side = torch.cuda.Stream()
+    rng = np.random.default_rng(4)
+    names = ["obs", "global_state", "rewards", "dones", "masks", "tracking_error", "step"]
+    pending = None
+    for s in range(8):
+        acts = random_legal_actions(ora.outputs()["masks"], rng)
+        ora.step(acts)
+        gpu.step(acts)
+        if pending is not None:  # the previous step's async copy, read after this step ran
+            side.synchronize()
+            host, want = pending
+            for k in names:
+                np.testing.assert_allclose(host[k].numpy(), want[k], rtol=TIGHT_RTOL, atol=1e-12, err_msg=k)
+        want = {k: v.copy() for k, v in ora.outputs().items()}
+        host = {k: torch.empty(want[k].shape, dtype=torch.from_numpy(want[k]).dtype, pin_memory=True)
+                for k in names}
+        gpu.copy_outputs_async(host, side.cuda_stream)
+        pending = (host, want)
+        rep = check_state(ora, gpu, Report(), f"db{s}", outputs=False)
+        assert rep.ok(TIGHT_RTOL), rep
+    side.synchronize()
+    gpu.set_output_buffers(1)
+    compare_outputs(gpu.host_outputs(), ora.outputs(), rep := Report(), tag="single")
+    assert rep.ok(TIGHT_RTOL), rep
