@@ -985,8 +985,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll
     for (int q = 0; q < PPT; ++q) L[q] = 0.0;
     float* mb = reinterpret_cast<float*>(R.buf());  // per-stage warp maxima, [stage * 32 + warp]
-#pragma unroll 1
-    for (int j = 0; j < nm; ++j) {
+    // one stage: every particle's log-likelihood for measurement j, added to L in
+    // stage order, and the stage's warp maximum (rounded up to fp32)
+    auto stage = [&](int j) {
       const double* m = S.meas + kMeasStride * ml[j];
       const double ox = m[0], oy = m[1], r2 = m[2], c2 = m[4];
       float mj = -CUDART_INF_F;
@@ -1007,7 +1008,14 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       key = __reduce_max_sync(0xffffffffu, key);
       key ^= (key >> 31) & 0x7fffffff;
       if (lane == 0) mb[j * 32 + warp] = __int_as_float(key);
+    };
+    // two stages per iteration so their distance / sqrt chains interleave
+#pragma unroll 1
+    for (int j = 0; j + 1 < nm; j += 2) {
+      stage(j);
+      stage(j + 1);
     }
+    if (nm & 1) stage(nm - 1);
     __syncthreads();
     double shift = 0.0;  // sum_j s'_j, in stage order
 #pragma unroll 1
