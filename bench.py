@@ -33,12 +33,42 @@ CONFIGS = {
     "c5": dict(desc="5v5 estimator-heavy (every pair pinged, every link up)", n_agents=5, n_targets=5,
                target_speed_frac=0.6, d_min=100.0, spawn_max_sep=400.0, horizon=128,
                comm_drop_prob=0.0, detection_range=1e9, comm_range=1e9, envs=131072),
+    # per-env fleet (A_i, T_i) ~ U{1..8}^2 keyed by derive_key(seed, "mix", i),
+    # padded to 8 x 8 in the batch buffers, ragged particle storage. 262,144 envs need
+    # ~218 GB of particles, so one GPU runs 65,536 (the 8-GPU run holds the full mix).
+    "c4": dict(desc="curriculum mix: 1-8 agents x 1-8 targets per env (padded 8x8, ragged particles)",
+               n_agents=8, n_targets=8, spawn_max_sep=600.0, horizon=128, envs=65536, mix=True),
 }
+MIX_TAG = 0x6d6978  # "mix"
 
 
-def make_cfg(name, particles=1024):
+def mix_fleet(lo, hi, seed=0):
+    """(A_i, T_i) for global envs [lo, hi): the low 6 bits of derive_key(seed, "mix", i)
+    (rng.hpp:30-38) as two 3-bit fields."""
+    def splitmix(x):
+        x = (x + 0x9e3779b97f4a7c15) & (2**64 - 1)
+        x = ((x ^ (x >> 30)) * 0xbf58476d1ce4e5b9) & (2**64 - 1)
+        x = ((x ^ (x >> 27)) * 0x94d049bb133111eb) & (2**64 - 1)
+        return x ^ (x >> 31)
+
+    def derive(a, b, c, d=0):
+        h = 0x9e3779b97f4a7c15
+        for v in (a, b, c, d):
+            h ^= splitmix((v + h) & (2**64 - 1))
+            h = ((h << 23) | (h >> 41)) & (2**64 - 1)
+        return splitmix(h)
+    out = []
+    for i in range(lo, hi):
+        h = derive(seed, MIX_TAG, i)
+        out.append((1 + (h & 7), 1 + ((h >> 3) & 7)))
+    return out
+
+
+def make_cfg(name, particles=1024, n_agents=None, n_targets=None):
     from paper_2505_08222_b200.vecenv import EnvConfig, PfConfig
-    kw = {k: v for k, v in CONFIGS[name].items() if k not in ("desc", "envs")}
+    kw = {k: v for k, v in CONFIGS[name].items() if k not in ("desc", "envs", "mix")}
+    if n_agents is not None:
+        kw.update(n_agents=n_agents, n_targets=n_targets)
     return EnvConfig(**kw, pf=PfConfig(n_particles=particles))
 
 
@@ -247,7 +277,18 @@ def main():
     per_gpu = args.envs_per_gpu or CONFIGS[args.config]["envs"]
     total = per_gpu * world
     lo, hi = shard_range(total, rank, world)
-    venv = VecEnv(cfg, hi - lo, master_seed=0, env_index_offset=lo, device=local)
+    if CONFIGS[args.config].get("mix"):
+        fleets = mix_fleet(lo, hi)
+        shapes = [(a, t) for a in range(1, 9) for t in range(1, 9)]
+        cfgs = [make_cfg(args.config, args.particles, a, t) for a, t in shapes]
+        venv = VecEnv(cfgs, hi - lo, master_seed=0, env_index_offset=lo, device=local,
+                      fleet=[shapes.index(f) for f in fleets])
+        agents_local = sum(a for a, _ in fleets)
+        pf_bytes_local = sum(80 * P * a * t for a, t in fleets)
+    else:
+        venv = VecEnv(cfg, hi - lo, master_seed=0, env_index_offset=lo, device=local)
+        agents_local = (hi - lo) * A
+        pf_bytes_local = (hi - lo) * 80 * P * A * T
     stream = torch.cuda.current_stream()
     venv.set_stream(stream.cuda_stream)
 
@@ -273,7 +314,11 @@ def main():
     ms_max = float(t.item())
     secs = ms_max / 1e3
     env_steps = total * args.steps
-    value = env_steps * A / secs
+    ag = torch.tensor([float(agents_local)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ag)
+    agents_total = float(ag.item())  # = total * A for a homogeneous fleet
+    value = agents_total * args.steps / secs
 
     # episode statistics: the one NCCL collective (north_star)
     st = torch.tensor(venv.stats(), dtype=torch.float64, device="cuda")
@@ -334,10 +379,12 @@ def main():
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = total * e2e_steps * A / float(te.item())
+    e2e_value = agents_total * e2e_steps / float(te.item())
 
     peak, peak_kind = measured_peaks()
-    bytes_launch = algorithmic_bytes_per_env_step(A, T, P, rec_words_for(A, T)) * (hi - lo)
+    # particle bytes of this shard's fleet + record and (padded) outputs per env
+    per_env_rest = algorithmic_bytes_per_env_step(A, T, P, rec_words_for(A, T)) - 80 * P * A * T
+    bytes_launch = pf_bytes_local + per_env_rest * (hi - lo)
     avg_launch_s = secs / max(1, args.steps)
     achieved = bytes_launch / avg_launch_s / 1e9
 
