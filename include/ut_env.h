@@ -225,6 +225,16 @@ int ut_env_deserialize(ut_vecenv* v, int64_t env, const double* blob, size_t len
 int ut_vecenv_export_state(ut_vecenv* v, int64_t env_begin, int64_t env_end, double* blobs, size_t cap,
                            size_t* len);
 int ut_vecenv_import_state(ut_vecenv* v, int64_t env_begin, int64_t env_end, const double* blobs, size_t len);
+/* Trajectory capture (append_trajectory_rows, trajectory.cpp:13-66; used by
+ * curriculum::evaluate and cmd_rollout) for envs [env_begin, env_end) (empty =
+ * off): every step, before auto-reset, each captured env records one row per
+ * entity -- agents then targets, padded to the batch's rows -- of
+ * UT_TRAJ_FIELDS doubles: step (-1 on padding rows), x, y, z, heading,
+ * has_estimate, est_x, est_y, track_err, reward, collision, is_target.
+ * ut_vecenv_trajectory_rows copies the last step's rows (len = n x rows x fields). */
+enum { UT_TRAJ_FIELDS = 12 };
+int ut_vecenv_capture_trajectory(ut_vecenv* v, int64_t env_begin, int64_t env_end);
+int ut_vecenv_trajectory_rows(ut_vecenv* v, double* rows, size_t cap, size_t* len);
 /* world().step (env.hpp:50), read by Trainer::collect_rollout (marl.cpp:211,227). */
 int ut_env_world_step(ut_vecenv* v, int64_t env, int32_t* step);
 

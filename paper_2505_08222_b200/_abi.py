@@ -7,6 +7,7 @@ import ctypes as C
 
 UT_OK, UT_ERR_CONTRACT, UT_ERR_CONFIG, UT_ERR_DATA, UT_ERR_RUNTIME = 0, 1, 2, 3, 4
 UT_NUM_ACTIONS = 5
+UT_TRAJ_FIELDS = 12
 UT_FEATURE_DIM = 12
 UT_REWARD_TRACKING, UT_REWARD_FOLLOW = 0, 1
 UT_POLICY_RANDOM, UT_POLICY_SCRIPTED = 0, 1
@@ -108,6 +109,8 @@ def declare_product(lib):
         "ut_vecenv_copy_outputs": (C.c_int, [P, C.POINTER(HostOutputs)]),
         "ut_vecenv_set_stream": (C.c_int, [P, P]),
         "ut_vecenv_set_output_buffers": (C.c_int, [P, C.c_int]),
+        "ut_vecenv_capture_trajectory": (C.c_int, [P, I64, I64]),
+        "ut_vecenv_trajectory_rows": (C.c_int, [P, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_size_t)]),
         "ut_vecenv_copy_outputs_async": (C.c_int, [P, C.POINTER(HostOutputs), P]),
         "ut_vecenv_synchronize": (C.c_int, [P]),
         "ut_vecenv_stats": (C.c_int, [P, C.POINTER(C.c_double), C.c_int]),
@@ -157,7 +160,7 @@ PRODUCT_SYMBOLS = (
     "ut_vecenv_set_stream", "ut_vecenv_synchronize", "ut_vecenv_stats", "ut_vecenv_launch_count",
     "ut_env_serialize", "ut_env_deserialize", "ut_env_world_step", "ut_benchmark_sps",
     "ut_vecenv_export_state", "ut_vecenv_import_state", "ut_vecenv_set_output_buffers",
-    "ut_vecenv_copy_outputs_async",
+    "ut_vecenv_copy_outputs_async", "ut_vecenv_capture_trajectory", "ut_vecenv_trajectory_rows",
     "ut_vecenv_enable_phase_timing", "ut_vecenv_phase_cycles",
     "ut_last_error", "ut_abi_version",
 )

@@ -371,6 +371,8 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   B.error_info = nullptr;
   B.force_exact = 0;
   B.trace_env = -1;
+  B.traj = nullptr;
+  B.traj_lo = B.traj_hi = 0;
   B.phase_cycles = nullptr;
   // VecEnv ctor zero-fills every batch buffer (vecenv.cpp:26-38)
   UT_CUDA(cudaMemsetAsync(B.final_obs, 0, sizeof(double) * 12 * B.obs_rows, v->stream));
@@ -651,6 +653,37 @@ int ut_vecenv_copy_outputs_async(ut_vecenv* v, const ut_host_outputs* d, void* c
   UT_CUDA(cp(d->collision, B.collision, (size_t)n));
   UT_CUDA(cp(d->step, B.step, sizeof(int32_t) * n));
   UT_CUDA(cudaEventRecord(done, cs));
+  return UT_OK;
+}
+
+int ut_vecenv_capture_trajectory(ut_vecenv* v, int64_t env_begin, int64_t env_end) {
+  if (env_begin < 0 || env_end > v->n_envs || env_begin > env_end)
+    return fail(UT_ERR_CONTRACT, "capture_trajectory: env range [%lld, %lld) outside [0, %lld)",
+                (long long)env_begin, (long long)env_end, (long long)v->n_envs);
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  if (v->B.traj) {
+    cudaFree(v->B.traj);
+    v->allocs.erase(std::remove(v->allocs.begin(), v->allocs.end(), (void*)v->B.traj), v->allocs.end());
+    v->B.traj = nullptr;
+  }
+  v->B.traj_lo = env_begin;
+  v->B.traj_hi = env_end;
+  if (env_end > env_begin) {
+    int rc;
+    if ((rc = v->alloc(&v->B.traj, (size_t)((env_end - env_begin) * v->R_max * kTrajFields)))) return rc;
+    UT_CUDA(cudaMemset(v->B.traj, 0, sizeof(double) * (env_end - env_begin) * v->R_max * kTrajFields));
+  }
+  return v->sync_batch();
+}
+
+int ut_vecenv_trajectory_rows(ut_vecenv* v, double* rows, size_t cap, size_t* len) {
+  const size_t need = (size_t)((v->B.traj_hi - v->B.traj_lo) * v->R_max * kTrajFields);
+  *len = need;
+  if (!rows) return UT_OK;
+  if (cap < need) return fail(UT_ERR_DATA, "trajectory_rows: buffer of %zu doubles too small (need %zu)", cap, need);
+  if (need == 0) return UT_OK;
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  UT_CUDA(cudaMemcpy(rows, v->B.traj, need * sizeof(double), cudaMemcpyDeviceToHost));
   return UT_OK;
 }
 

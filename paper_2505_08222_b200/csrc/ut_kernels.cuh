@@ -301,6 +301,45 @@ __device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B,
 
 // compute_reward_and_info (env.cpp:473-505) + VecEnv bookkeeping
 // (vecenv.cpp:95-104) + device statistics for env e. Returns done.
+// append_trajectory_rows (trajectory.cpp:13-66) for env e after its step: agents,
+// then targets with the best-informed track (first agent with the smallest
+// error, as the reward attributes it) and this step's tracking error.
+__device__ __noinline__ void write_trajectory(const DevConfig& c, const DevBatch& B, int64_t e, double reward,
+                                              bool crash, double step) {
+  const Rec rec = rec_of(B, e);
+  const int A = c.A, T = c.T;
+  double* out = B.traj + (e - B.traj_lo) * (int64_t)B.R_max * kTrajFields;
+  for (int r = 0; r < B.R_max; ++r) {
+    double* row = out + (int64_t)r * kTrajFields;
+    for (int f = 0; f < kTrajFields; ++f) row[f] = 0.0;
+    row[TJ_STEP] = r < A + T ? step : -1.0;  // -1: padding row of a smaller fleet
+    if (r >= A + T) continue;
+    const bool tgt = r >= A;
+    const int i = tgt ? r - A : r;
+    row[TJ_X] = tgt ? TG(V_X, i) : AG(V_X, i);
+    row[TJ_Y] = tgt ? TG(V_Y, i) : AG(V_Y, i);
+    row[TJ_Z] = tgt ? TG(V_Z, i) : AG(V_Z, i);
+    row[TJ_HEAD] = tgt ? TG(V_HEAD, i) : AG(V_HEAD, i);
+    row[TJ_REWARD] = reward;
+    row[TJ_COLLISION] = crash ? 1.0 : 0.0;
+    row[TJ_IS_TARGET] = tgt ? 1.0 : 0.0;
+    if (tgt) {
+      double best = CUDART_INF;
+      for (int a = 0; a < A; ++a) {
+        const int ti = a * c.sT + i;
+        const double d = norm2(TRK(K_EX, ti) - TG(V_X, i), TRK(K_EY, ti) - TG(V_Y, i));
+        if (d < best) {
+          best = d;
+          row[TJ_HAS_EST] = 1.0;
+          row[TJ_EST_X] = TRK(K_EX, ti);
+          row[TJ_EST_Y] = TRK(K_EY, ti);
+        }
+      }
+      row[TJ_ERR] = best;  // out.tracking_error[t] (step > 0)
+    }
+  }
+}
+
 __device__ __noinline__ bool env_epilogue(const DevConfig& c, const DevBatch& B, int64_t e) {
   const Rec rec = rec_of(B, e);
   const int A = c.A, T = c.T, Tm = B.T_max;
@@ -367,6 +406,7 @@ __device__ __noinline__ bool env_epilogue(const DevConfig& c, const DevBatch& B,
   STAT(5) += crash ? 1.0 : 0.0;
   STAT(6) += lost_n;
   rec[R_EP_RETURN] += reward;
+  if (B.traj && e >= B.traj_lo && e < B.traj_hi) write_trajectory(c, B, e, reward, crash, step);
   // evaluation accumulators (curriculum.cpp:307-325, agents outer over targets
   // there; here targets outer -- a different summation order of the same terms)
   rec[R_EV_DIST] += dist_all;

@@ -117,10 +117,20 @@ struct DevBatch {
   // Phase timing (PhaseTimer, env.cpp:18-36): SM cycles per CTA accumulated in
   // [grid][kPhaseCount] when non-null.
   unsigned long long* phase_cycles;
+  // Trajectory capture (append_trajectory_rows, trajectory.cpp:13-66) for envs
+  // [traj_lo, traj_hi): after every step, before auto-reset, env e writes R_max
+  // rows of kTrajFields doubles at traj[((e - traj_lo) * R_max + row) * kTrajFields].
+  double* traj;
+  int64_t traj_lo, traj_hi;
   // Device copy of this struct, for the out-of-line (cold) device functions, so
   // the kernel's by-value parameter is never address-taken.
   const struct DevBatch* self;
 };
+
+// Trajectory row fields (TrajectoryRow, trajectory.hpp:13-21): step, x, y, z,
+// heading, has_estimate, est_x, est_y, track_err, reward, collision, is_target.
+enum : int { TJ_STEP = 0, TJ_X, TJ_Y, TJ_Z, TJ_HEAD, TJ_HAS_EST, TJ_EST_X, TJ_EST_Y, TJ_ERR, TJ_REWARD,
+             TJ_COLLISION, TJ_IS_TARGET, kTrajFields };
 
 // Device phases (the reference's seven StepPhase values, env.hpp:71-80, map onto
 // these: targets+agents+measure+comm decisions -> PROLOGUE, filter+comm updates

@@ -371,6 +371,20 @@ class VecEnv:
         _check(self._lib.ut_vecenv_import_state(self._h, begin, end, b.ctypes.data_as(C.POINTER(C.c_double)),
                                                 b.size))
 
+    def capture_trajectory(self, begin: int, end: int):
+        """Record append_trajectory_rows (trajectory.cpp:13-66) for envs [begin,
+        end) after every step, before auto-reset (empty range: off)."""
+        _check(self._lib.ut_vecenv_capture_trajectory(self._h, begin, end))
+
+    def trajectory_rows(self) -> np.ndarray:
+        """The last step's captured rows: (n_captured, n_rows, UT_TRAJ_FIELDS)."""
+        n = C.c_size_t()
+        _check(self._lib.ut_vecenv_trajectory_rows(self._h, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.float64)
+        _check(self._lib.ut_vecenv_trajectory_rows(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), n.value,
+                                                   C.byref(n)))
+        return out.reshape(-1, self._b.n_rows, _abi.UT_TRAJ_FIELDS)
+
     def world_step(self, env: int) -> int:
         s = C.c_int32()
         _check(self._lib.ut_env_world_step(self._h, env, C.byref(s)))

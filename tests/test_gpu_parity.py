@@ -359,3 +359,50 @@ def test_output_double_buffering_and_async_copies(cuda_device):
     gpu.set_output_buffers(1)
     compare_outputs(gpu.host_outputs(), ora.outputs(), rep := Report(), tag="single")
     assert rep.ok(TIGHT_RTOL), rep
+
+
+def test_trajectory_capture_matches_state(cuda_device, tmp_path):
+    """ut_vecenv_capture_trajectory == append_trajectory_rows (trajectory.cpp:13-66)
+    computed from the oracle's state after each step; the terminal step is
+    captured before the auto-reset; CSV in the reference layout."""
+    from paper_2505_08222_b200.trajectory import HEADER, write_trajectory_csv
+    A, T, P = 2, 3, 64
+    kw = dict(n_agents=A, n_targets=T, pf_n_particles=P, horizon=5, spawn_max_sep=400.0)
+    cfg, ora, gpu = make_pair(kw, 4, 17)
+    gpu.capture_trajectory(1, 3)
+    rng = np.random.default_rng(2)
+    steps = []
+    for s in range(5):
+        acts = random_legal_actions(ora.outputs()["masks"], rng)
+        ora.step(acts)
+        gpu.step(acts)
+        rows = gpu.trajectory_rows()
+        assert rows.shape == (2, A + T, 12)
+        steps.append(rows[0].copy())
+        out = gpu.host_outputs()
+        for i, e in enumerate((1, 2)):
+            assert np.all(rows[i, :, 0] == s + 1)
+            np.testing.assert_array_equal(rows[i, :, 9], out["rewards"][e])
+            np.testing.assert_array_equal(rows[i, A:, 8], out["tracking_error"][e * T:(e + 1) * T])
+            if s == 4:
+                continue  # terminal step: the state has been reset since
+            b = ora.serialize(e)
+            base = lambda a: 5 + 6 * A + 9 * T + a * (6 * A + T * (9 + 5 * P))
+            for a in range(A):
+                np.testing.assert_allclose(rows[i, a, 1:5], b[5 + 6 * a:5 + 6 * a + 4], rtol=TIGHT_RTOL, atol=1e-12)
+            for t in range(T):
+                tv = b[5 + 6 * A + 8 * t:5 + 6 * A + 8 * t + 4]
+                np.testing.assert_allclose(rows[i, A + t, 1:5], tv, rtol=TIGHT_RTOL, atol=1e-12)
+                ests = [b[base(a) + 6 * A + t * (9 + 5 * P):][:2] for a in range(A)]
+                errs = [np.sqrt((ex - tv[0]) ** 2 + (ey - tv[1]) ** 2) for ex, ey in ests]
+                best = int(np.argmin(errs))
+                np.testing.assert_allclose(rows[i, A + t, 6:8], ests[best], rtol=TIGHT_RTOL, atol=1e-12)
+                assert rows[i, A + t, 5] == 1 and rows[i, A + t, 11] == 1
+    path = tmp_path / "traj" / "episode_0001.csv"
+    write_trajectory_csv(str(path), steps)
+    lines = path.read_text().splitlines()
+    assert lines[0] == HEADER and len(lines) == 1 + 5 * (A + T)
+    assert all(len(ln.split(",")) == 12 for ln in lines)
+    assert lines[1].startswith("1,agent_0,agent,") and lines[A + 1].startswith("1,target_0,target,")
+    gpu.capture_trajectory(0, 0)
+    assert gpu.trajectory_rows().size == 0
