@@ -406,3 +406,16 @@ def test_trajectory_capture_matches_state(cuda_device, tmp_path):
     assert lines[1].startswith("1,agent_0,agent,") and lines[A + 1].startswith("1,target_0,target,")
     gpu.capture_trajectory(0, 0)
     assert gpu.trajectory_rows().size == 0
+
+
+def test_c3_at_scale_against_oracle(cuda_device):
+    """C3 (5 agents vs 5 fast targets, P = 1024) on 96 envs for 16 steps: every
+    output each step and every state word at the end against the oracle."""
+    cfg, ora, gpu = make_pair(dict(CONFIGS["c3_5v5_fast"], horizon=128), 96, 7)
+    rep = Report()
+    for s in range(16):
+        ora.step_policy(1)
+        gpu.step_policy("random", 1)
+        compare_outputs(gpu.host_outputs(), ora.outputs(), rep, tag=f"s{s}")
+    check_state(ora, gpu, rep, "final", outputs=False)
+    assert rep.ok(TIGHT_RTOL), rep
