@@ -176,6 +176,18 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def fp64_peak_per_s(device):
+    """Measured thread-level DFMA issue rate of this device (ut_debug_fp64_peak)."""
+    import ctypes as C
+    from paper_2505_08222_b200 import _native, _abi
+    lib = _native.lib()
+    _abi.declare_debug(lib)
+    out = C.c_double()
+    if lib.ut_debug_fp64_peak(device, C.byref(out)) != 0:
+        return None
+    return out.value
+
+
 def cpu_baseline(cfg_name, particles, budget_s=12.0):
     """The reference's own benchmark_sps (vecenv.cpp:175-202), compiled from its
     sources into oracle/_ref, on this host's cores over a bounded sample."""
@@ -298,6 +310,7 @@ def main():
         dist.barrier()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = venv.launch_count()
+    upd0 = float(venv.stats()[STAT_NAMES.index("pf_updates")])
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         if world > 1:
@@ -307,6 +320,7 @@ def main():
         end.record(stream)
         torch.cuda.synchronize()
     gpu_launches = venv.launch_count() - launches0
+    upd_timed = float(venv.stats()[STAT_NAMES.index("pf_updates")]) - upd0
     ms = start.elapsed_time(end)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -387,6 +401,13 @@ def main():
     bytes_launch = pf_bytes_local + per_env_rest * (hi - lo)
     avg_launch_s = secs / max(1, args.steps)
     achieved = bytes_launch / avg_launch_s / 1e9
+    # SURVEY 8d fp64 component: 39 + 55 u algorithmic fp64 instructions per
+    # particle per step (u = range updates applied to its set this step, counted
+    # by the kernel), against the device's measured DFMA issue rate.
+    sets_local = pf_bytes_local // (80 * P)
+    fp64_launch = P * (39.0 * sets_local * args.steps + 55.0 * upd_timed) / args.steps
+    fp64_peak = fp64_peak_per_s(local)
+    fp64_achieved = fp64_launch / avg_launch_s
 
     line = {
         "metric": "agent-env steps/sec (5v5 fast targets)" if args.config == "c3" else f"agent-env steps/sec ({args.config})",
@@ -402,7 +423,16 @@ def main():
                      "traffic": args.traffic_bytes if args.traffic_bytes is not None
                      else measured_traffic(args.config, per_gpu, P),
                      "kernel": "step_kernel<4,1024,FULL>", "bytes_per_launch": bytes_launch,
-                     "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_kind},
+                     "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_kind,
+                     "components": {
+                         "hbm": {"achieved_gbs": achieved, "peak_gbs": peak, "frac": achieved / peak},
+                         "fp64": {"achieved_tinstr_s": fp64_achieved / 1e12,
+                                  "peak_tinstr_s": fp64_peak / 1e12 if fp64_peak else None,
+                                  "frac": fp64_achieved / fp64_peak if fp64_peak else None,
+                                  "instr_per_launch": fp64_launch,
+                                  "updates_per_set_step": upd_timed / max(1, sets_local * args.steps),
+                                  "model": "39 + 55 u fp64 instr per particle-step (SURVEY 8d)",
+                                  "peak_source": "ut_debug_fp64_peak (8 DFMA chains/thread)"}}},
         "gpu_launches": gpu_launches,
         "clocks": clocks.summary(),
         "stats": {k: float(v) for k, v in zip(STAT_NAMES, st)},

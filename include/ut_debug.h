@@ -27,6 +27,9 @@ int ut_debug_set_knobs(struct ut_vecenv* v, int force_exact, int64_t trace_env);
 /* sizeof of the ABI structs as compiled: ut_env_config, ut_buffers,
  * ut_host_outputs, ut_benchmark_report (no device needed). */
 int ut_debug_abi_sizes(int64_t out[4]);
+/* Measured fp64 issue peak of the device: thread-level DFMA per second from 8
+ * independent chains per thread on 8 CTAs of 256 threads per SM (best of 5). */
+int ut_debug_fp64_peak(int device, double* dfma_per_s);
 /* derive_key (rng.hpp:30-38) evaluated on the device. */
 int ut_debug_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t d, int device, uint64_t* out);
 #ifdef __cplusplus

@@ -1119,6 +1119,21 @@ __global__ void philox_kernel(uint64_t key, uint64_t stream, uint64_t block0, in
 __global__ void derive_key_kernel(uint64_t a, uint64_t b, uint64_t c, uint64_t d, uint64_t* out) {
   *out = derive_key(a, b, c, d);
 }
+// FP64 issue peak: 8 independent DFMA chains per thread (the denominator of the
+// step kernel's fp64 roofline).
+__global__ void __launch_bounds__(256) fp64_peak_kernel(int iters, double seed, double* sink) {
+  double a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = seed + 1e-9 * (double)threadIdx.x + (double)j;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = fma(a[j], 0.9999999, 1e-7);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s = s + a[j];
+  if (s == 12345.0) *sink = s;
+}
 }  // namespace
 
 #include "ut_debug.h"
@@ -1172,6 +1187,35 @@ int ut_debug_philox(uint64_t key, uint64_t stream, uint64_t block0, int32_t n, i
   cudaError_t err = cudaMemcpy(host_out, d, (size_t)n * sizeof(uint4), cudaMemcpyDeviceToHost);
   cudaFree(d);
   UT_CUDA(err);
+  return UT_OK;
+}
+int ut_debug_fp64_peak(int device, double* dfma_per_s) {
+  UT_CUDA(cudaSetDevice(device));
+  int sms = 0;
+  UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  double* d = nullptr;
+  UT_CUDA(cudaMalloc(&d, sizeof(double)));
+  cudaEvent_t e0, e1;
+  UT_CUDA(cudaEventCreate(&e0));
+  UT_CUDA(cudaEventCreate(&e1));
+  const int blocks = sms * 8, iters = 1 << 14;
+  fp64_peak_kernel<<<blocks, 256>>>(64, 1.0, d);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    fp64_peak_kernel<<<blocks, 256>>>(iters, 1.0, d);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = ms < best ? ms : best;
+  }
+  cudaError_t err = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  UT_CUDA(err);
+  *dfma_per_s = (double)blocks * 256.0 * (double)iters * 8.0 / (best * 1e-3);
   return UT_OK;
 }
 int ut_debug_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t dd, int device, uint64_t* out) {

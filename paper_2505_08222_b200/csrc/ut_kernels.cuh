@@ -728,16 +728,20 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   int* mark = reinterpret_cast<int*>(S.cum);  // [P] source marks of the outputs
   double* st = S.st;
   double* wsum = S.red + 2 * kRedSlots;  // [32] warp totals, then [32] int warp maxima at +96
+  // Staging layout: particle k = k0 + q of thread t at q * NT + t, so each
+  // field's stores are lane-contiguous (conflict-free); a field spans FS slots.
+  const int NT = NW > 0 ? NW * 32 : (int)blockDim.x;
+  const int FS = NT * PPT;
   double loc[PPT];
   double run = 0.0;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     const int k = k0 + q;
     if (FULL || k < P) {
-      st[k] = s.px[q];
-      st[P + k] = s.py[q];
-      st[2 * P + k] = s.vx[q];
-      st[3 * P + k] = s.vy[q];
+      st[q * NT + tid] = s.px[q];
+      st[FS + q * NT + tid] = s.py[q];
+      st[2 * FS + q * NT + tid] = s.vx[q];
+      st[3 * FS + q * NT + tid] = s.vy[q];
       run = q == 0 ? s.w[q] : run + s.w[q];
     }
     loc[q] = run;
@@ -752,9 +756,8 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   double excl = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) excl = 0.0;
   if (lane == 31) wsum[warp] = incl;
-#pragma unroll
-  for (int q = 0; q < PPT; ++q)
-    if (FULL || k0 + q < P) mark[k0 + q] = 0;
+  static_assert(PPT == 4, "mark zeroing assumes 4 particles per thread");
+  if (FULL || k0 < P) *reinterpret_cast<int4*>(mark + k0) = make_int4(0, 0, 0, 0);
   __syncthreads();
   double woff = 0.0;  // cum[k] = (sum of earlier warps' totals + excl) + loc[q]
   if constexpr (NW > 0) {
@@ -781,20 +784,27 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
     if (m < P && ((double)m + u0) * inv_n <= cv) ++m;
     return m;
   };
+  int hq[PPT];  // count(cum[k]); P = no mark (the last particle, padding)
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) hq[q] = k0 + q < P - 1 ? count_le(base + loc[q]) : P;
+  // Of a run of consecutive particles with the same count only the last one's
+  // mark survives the max, so only it issues the atomic (lane 31's last always
+  // does): the same marks with ~P spread atomics instead of P + conflicts.
+  int nxt = __shfl_down_sync(0xffffffffu, hq[0], 1);
+  if (lane == 31) nxt = -1;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
-    const int k = k0 + q;
-    if (k < P - 1) {
-      const int hi = count_le(base + loc[q]);
-      if (hi < P) atomicMax(&mark[hi], k + 1);
-    }
+    const int hn = q + 1 < PPT ? hq[q + 1] : nxt;
+    if (hq[q] < P && hq[q] != hn) atomicMax(&mark[hq[q]], k0 + q + 1);
   }
   __syncthreads();
   int r[PPT];
-#pragma unroll
-  for (int q = 0; q < PPT; ++q) {
-    r[q] = (FULL || k0 + q < P) ? mark[k0 + q] : 0;
-    if (q > 0) r[q] = max(r[q], r[q - 1]);
+  {
+    const int4 m4 = (FULL || k0 < P) ? *reinterpret_cast<const int4*>(mark + k0) : make_int4(0, 0, 0, 0);
+    r[0] = m4.x;
+    r[1] = max(m4.y, r[0]);
+    r[2] = max(m4.z, r[1]);
+    r[3] = max(m4.w, r[2]);
   }
   int mi = r[PPT - 1];
 #pragma unroll
@@ -818,10 +828,11 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   for (int q = 0; q < PPT; ++q) {
     if (FULL || k0 + q < P) {
       const int i = max(mex, r[q]);
-      s.px[q] = st[i];
-      s.py[q] = st[P + i];
-      s.vx[q] = st[2 * P + i];
-      s.vy[q] = st[3 * P + i];
+      const int j = (i & (PPT - 1)) * NT + i / PPT;
+      s.px[q] = st[j];
+      s.py[q] = st[FS + j];
+      s.vx[q] = st[2 * FS + j];
+      s.vy[q] = st[3 * FS + j];
       s.w[q] = inv_n;
     }
   }
