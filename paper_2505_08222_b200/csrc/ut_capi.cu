@@ -309,6 +309,10 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
     v->set_off[(size_t)e] = v->total_sets;
     v->total_sets += (int64_t)d.A * d.T;
   }
+  // the step kernel indexes envs and particle sets in 32 bits
+  if (v->total_sets >= ((int64_t)1 << 31) - 1)
+    return fail(UT_ERR_CONFIG, "n_envs x agents x targets = %lld particle sets per device (max 2^31 - 2)",
+                (long long)v->total_sets);
 
   UT_CUDA(cudaSetDevice(device));
   UT_CUDA(cudaStreamCreateWithFlags(&v->own_stream, cudaStreamNonBlocking));

@@ -858,8 +858,9 @@ __device__ __forceinline__ void prefetch_set(const DevBatch& B, const Smem& S, i
 // (phase `tphase`), the Philox blocks are computed in registers and the next
 // set `next` (>= 0) is prefetched into S.pf after this set's last barrier.
 template <int PPT, bool FULL, int NW>
-__device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, const Rec& rec,
-                         int64_t gi, int64_t gset, int a, int t, uint32_t& tphase, int64_t next) {
+__device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int e, int gset,
+                         int a, int t, uint32_t& tphase, int next) {
+  const Rec rec = rec_of(B, e);
   const int P = c.P, tid = threadIdx.x, T = c.T;
   const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int ps = a * T + t;     // PF stream id / set within the env (env.cpp:130-133)
@@ -1155,9 +1156,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     }
   }
 
-  if (B.trace_env == gi - B.env_index_offset && tid == 0)
+  if (B.trace_env == (int64_t)e && tid == 0)
     printf("[trace env %lld set %d] nm=%d exact=%d have_ess=%d ess=%.17g resampled=%d pos=%llu\n",
-           (long long)(gi - B.env_index_offset), ps, nm, (int)exact, (int)have_ess, ess, (int)resampled,
+           (long long)e, ps, nm, (int)exact, (int)have_ess, ess, (int)resampled,
            (unsigned long long)pos);
 
   // ---- estimate (env.cpp:403-407)
@@ -1344,62 +1345,73 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
   BlockReducer R{S.red, 0};
   load_tables(S);
   if (FULL && threadIdx.x == 0) mbar_init(S.mbar, 1);
-  int64_t lo, hi;
-  cta_range(B.n_envs, lo, hi);
-  const int64_t set_end = hi < B.n_envs ? set_off(B, hi) : set_off(B, hi - 1) + cfg_of(B, hi - 1).A * cfg_of(B, hi - 1).T;
+  // env and set indices fit in 32 bits (checked at creation)
+  int lo, hi;
+  {
+    int64_t lo64, hi64;
+    cta_range(B.n_envs, lo64, hi64);
+    lo = (int)lo64, hi = (int)hi64;
+  }
+  const int set_end = (int)(hi < B.n_envs ? set_off(B, hi) : set_off(B, hi - 1) + cfg_of(B, hi - 1).A * cfg_of(B, hi - 1).T);
   __syncthreads();
   uint32_t tphase = 0;
-  long long cyc[kPhaseCount] = {0, 0, 0, 0};
-  for (int64_t e0 = lo; e0 < hi; e0 += blockDim.x) {
-    const int64_t e1 = min(hi, e0 + (int64_t)blockDim.x);
+  // phase timing (thread 0, shared memory: nothing live in registers)
+  __shared__ long long ph_cyc[kPhaseCount + 1];
+  const bool timing = B.phase_cycles != nullptr;
+  if (timing && threadIdx.x == 0)
+    for (int k = 0; k <= kPhaseCount; ++k) ph_cyc[k] = 0;
+  auto mark = [&](int k) {  // close phase k (k < 0: open the first)
+    if (timing && threadIdx.x == 0) {
+      const long long now = clock64();
+      if (k >= 0) ph_cyc[k] += now - ph_cyc[kPhaseCount];
+      ph_cyc[kPhaseCount] = now;
+    }
+  };
+  for (int e0 = lo; e0 < hi; e0 += blockDim.x) {
+    const int e1 = min(hi, e0 + (int)blockDim.x);
     // the chunk's sets [set_off(e0), chunk_end) are prefetched one ahead; the
     // set buffer is free at chunk boundaries (the reset phase uses it)
-    const int64_t chunk_end = e1 < B.n_envs ? set_off(B, e1) : set_end;
+    const int chunk_end = (int)(e1 < B.n_envs ? set_off(B, e1) : set_end);
     if (FULL && threadIdx.x == 0) prefetch_set(B, S, set_off(B, e0), B.P);
-    long long t0 = clock64();
+    mark(-1);
     // ---- 1. prologue, one env per thread
     {
-      const int64_t e = e0 + threadIdx.x;
+      const int e = e0 + threadIdx.x;
       if (e < e1) env_prologue(cfg_of(Bg, e), Bg, e, B.env_index_offset + e, mode);
     }
     __syncthreads();
-    long long t1 = clock64();
-    cyc[PH_PROLOGUE] += t1 - t0;
+    mark(PH_PROLOGUE);
     // ---- 2. every particle set of the chunk
-    for (int64_t e = e0; e < e1; ++e) {
-      const Rec rec = rec_of(B, e);
-      stage_env(cfg_of(B, e), B, S, rec, e);
+    for (int e = e0; e < e1; ++e) {
+      stage_env(cfg_of(B, e), B, S, rec_of(B, e), e);
       __syncthreads();
       const DevConfig& c = *S.cfg;
-      const int64_t gi = B.env_index_offset + e;
-      const int64_t so = set_off(B, e);
+      const int so = (int)set_off(B, e);
       const int nA = c.A, nT = c.T;
       for (int a = 0; a < nA; ++a)
         for (int t = 0; t < nT; ++t) {
-          const int64_t g = so + a * nT + t;
-          step_set<PPT, FULL, FULL ? NP / (32 * PPT) : 0>(c, B, S, R, rec, gi, g, a, t, tphase,
+          const int g = so + a * nT + t;
+          step_set<PPT, FULL, FULL ? NP / (32 * PPT) : 0>(c, B, S, R, e, g, a, t, tphase,
                                                            g + 1 < chunk_end ? g + 1 : -1);
         }
       __syncthreads();  // S.cfg / meas / mlist reused by the next env
     }
-    long long t2 = clock64();
-    cyc[PH_FILTER] += t2 - t1;
+    mark(PH_FILTER);
     // ---- 3. reward / done / info, one env per thread; then tokens
     {
-      const int64_t e = e0 + threadIdx.x;
+      const int e = e0 + threadIdx.x;
       if (e < e1) S.flags[threadIdx.x] = env_epilogue(cfg_of(Bg, e), Bg, e) ? kChunkFlagDone : 0;
     }
     __syncthreads();
     write_outputs(Bg, e0, e1, S.flags, 0, false);
     write_outputs(Bg, e0, e1, S.flags, kChunkFlagDone, true);  // terminal obs of finished envs
-    long long t3 = clock64();
-    cyc[PH_OUTPUT] += t3 - t2;
+    mark(PH_OUTPUT);
     // ---- 4. auto-reset of finished envs (vecenv.cpp:106-112)
     bool any = false;
     for (int i = 0; i < (int)(e1 - e0); ++i) any |= (S.flags[i] & kChunkFlagDone) != 0;
     if (any) {
       __syncthreads();
-      const int64_t e = e0 + threadIdx.x;
+      const int e = e0 + threadIdx.x;
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagDone)) {
         if (spawn_serial(cfg_of(Bg, e), Bg, e, B.env_index_offset + e))
           S.flags[threadIdx.x] |= kChunkFlagSpawned;
@@ -1413,10 +1425,10 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
     }
     if (FULL) fence_proxy_async();  // re-init words in the set buffer vs the next chunk's prefetch
     __syncthreads();
-    cyc[PH_RESET] += clock64() - t3;
+    mark(PH_RESET);
   }
-  if (B.phase_cycles && threadIdx.x == 0)
-    for (int k = 0; k < kPhaseCount; ++k) B.phase_cycles[blockIdx.x * kPhaseCount + k] += (unsigned long long)cyc[k];
+  if (timing && threadIdx.x == 0)
+    for (int k = 0; k < kPhaseCount; ++k) B.phase_cycles[blockIdx.x * kPhaseCount + k] += (unsigned long long)ph_cyc[k];
 }
 
 // Environment ctor / reset (env.cpp:110-151, 153-233) for every env. When
