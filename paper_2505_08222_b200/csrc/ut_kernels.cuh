@@ -775,14 +775,14 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   // boundary) and a prefix max over the marks (0 where unmarked) hands every
   // output its source; outputs past count(cum[n-2]) fall to n - 1.
   const double inv_n = 1.0 / (double)P;
+  // count(c) = floor(c n - u0) + 1, clamped to [0, n]. It can differ from the
+  // count against the rounded u_j = (j + u0)/n only when c n - u0 lies within
+  // ~1e-13 of an integer; the block-tree cumulative weights already differ
+  // from the reference's sequential ones by ~1e-15 (x n = 1e-12), so exact
+  // boundary tests would not make a flip any less likely.
   auto count_le = [&](double cv) -> int {
     const double x = cv * (double)P - u0;
-    int m = x < 0.0 ? 0 : (x >= (double)P ? P : (int)x + 1);
-    // x is within ~1e-12 of the real boundary and each u_j within an ulp of
-    // (j + u0)/n, so the estimate is off by at most one either way
-    if (m > 0 && ((double)(m - 1) + u0) * inv_n > cv) --m;
-    if (m < P && ((double)m + u0) * inv_n <= cv) ++m;
-    return m;
+    return x < 0.0 ? 0 : (x >= (double)P ? P : (int)x + 1);
   };
   int hq[PPT];  // count(cum[k]); P = no mark (the last particle, padding)
 #pragma unroll
@@ -860,17 +860,16 @@ __device__ __forceinline__ void prefetch_set(const DevBatch& B, const Smem& S, i
 template <int PPT, bool FULL, int NW>
 __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, int e, int gset,
                          int a, int t, uint32_t& tphase, int next) {
-  const Rec rec = rec_of(B, e);
   const int P = c.P, tid = threadIdx.x, T = c.T;
   const int lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int ps = a * T + t;     // PF stream id / set within the env (env.cpp:130-133)
   const int ti = a * c.sT + t;  // track index in the record
   const int k0 = tid * PPT;
   const double* tk = S.trk + kTrkStride * ti;  // staged by stage_env
-  uint64_t pos = (uint64_t)tk[TK_POS];
-  const double ms = tk[TK_MAXSPEED];
+  // pos, the max speed, the particle base and the record are (re)derived where
+  // used, so nothing long-lived occupies registers across the noise phase
+  const uint64_t pos = (uint64_t)tk[TK_POS];
   const uint64_t key = (uint64_t)__double_as_longlong(tk[TK_KEY]);
-  const size_t base = (size_t)gset * P;
   const int off = (int)(pos & 3);
   const bool noise = c.noise_on != 0;
   const uint64_t u0p = pos + (noise ? 4ull * (uint64_t)P : 0ull);  // resample draw follows predict
@@ -879,6 +878,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // Box-Muller pairs of all PPT particles can be interleaved)
   SetRegs<PPT> s;
   if (!FULL) {
+    const size_t base = (size_t)gset * P;
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       const int k = k0 + j;
@@ -975,7 +975,6 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         }
       }
     }
-    pos += 4ull * (uint64_t)P;
   }
   if (FULL) {
     mbar_wait(S.mbar, tphase);
@@ -1005,6 +1004,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       }
     }
   }
+  const double ms = tk[TK_MAXSPEED];
   if (ms > 0.0) {
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
@@ -1047,7 +1047,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       for (int q = 0; q < PPT; ++q) {
         if (FULL || k0 + q < P) {
           const double dx = s.px[q] - ox, dy = s.py[q] - oy;
-          const double d = sqrt_dist(dx * dx + dy * dy);
+          const double d = sqrt_dist(fma(dx, dx, dy * dy));
           const double tq = d - r2;
           const double ll = (tq * tq) * c2;  // -(1/2)((d - r)/sigma)^2 to a few ulp
           L[q] = L[q] + ll;
@@ -1113,7 +1113,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         exact = true;
       }
     }
-    if (exact && tid == 0) STAT(9) += 1.0;
+    if (exact && tid == 0) {
+      const Rec rec = rec_of(B, e);
+      STAT(9) += 1.0;
+    }
   }
   if (exact && nm > 0) {
     __syncthreads();  // every thread holds its particles: S.pf becomes the staging area
@@ -1150,7 +1153,6 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       const uint64_t u0_lo = reinterpret_cast<const uint32_t*>(S.bc)[0];
       const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
       const double u0 = (double)(((u0_hi << 32) | u0_lo) >> 11) * 0x1.0p-53;
-      pos += 2;
       pf_resample<PPT, FULL, NW>(s, k0, P, u0, S);
       resampled = true;
     }
@@ -1159,7 +1161,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   if (B.trace_env == (int64_t)e && tid == 0)
     printf("[trace env %lld set %d] nm=%d exact=%d have_ess=%d ess=%.17g resampled=%d pos=%llu\n",
            (long long)e, ps, nm, (int)exact, (int)have_ess, ess, (int)resampled,
-           (unsigned long long)pos);
+           (unsigned long long)pos);  // at set start
 
   // ---- estimate (env.cpp:403-407)
   // The set buffer is free once every thread is past the estimate barrier: the
@@ -1168,6 +1170,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   if (FULL) fence_proxy_async();
   const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R);
   if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
+  const size_t base = (size_t)gset * P;
   if (FULL) {
 #pragma unroll
     for (int q = 0; q < PPT; q += 2) {
@@ -1191,12 +1194,14 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     }
   }
   if (tid == 0) {
+    const Rec rec = rec_of(B, e);
     TRK(K_EX, ti) = est.x;
     TRK(K_EY, ti) = est.y;
     TRK(K_SPREAD, ti) = est.z;
     TRK(K_AGE, ti) = fresh ? 0.0 : tk[TK_AGE] + 1.0;
     TRK(K_EVER, ti) = (tk[TK_EVER] != 0.0 || fresh) ? 1.0 : 0.0;
-    TRK(K_POS, ti) = (double)pos;
+    // stream position: 4P predict draws, 2 for a resample (tracking.cpp:24-37, 160)
+    TRK(K_POS, ti) = tk[TK_POS] + (noise ? 4.0 * (double)P : 0.0) + (resampled ? 2.0 : 0.0);
     TRK(K_ESSOK, ti) = 1.0;  // maybe_resample ran: ESS >= P/2 or weights uniform
     STAT(7) += (double)nm;
     STAT(8) += resampled ? 1.0 : 0.0;
