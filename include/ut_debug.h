@@ -30,6 +30,11 @@ int ut_debug_abi_sizes(int64_t out[4]);
 /* Measured fp64 issue peak of the device: thread-level DFMA per second from 8
  * independent chains per thread on 8 CTAs of 256 threads per SM (best of 5). */
 int ut_debug_fp64_peak(int device, double* dfma_per_s);
+/* Cycles thread 0 of each CTA spent in each phase of the particle-set loop,
+ * summed over CTAs (12 slots: noise, TMA wait, load+predict, stages, shift,
+ * weight sums, exact/ESS, resample, store, estimate, tail). Non-zero only in
+ * builds with -DUT_SET_PROFILE (A/B diagnostics). */
+int ut_debug_set_profile(int device, uint64_t* out, int reset);
 /* derive_key (rng.hpp:30-38) evaluated on the device. */
 int ut_debug_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t d, int device, uint64_t* out);
 #ifdef __cplusplus

@@ -1222,6 +1222,21 @@ int ut_debug_fp64_peak(int device, double* dfma_per_s) {
   *dfma_per_s = (double)blocks * 256.0 * (double)iters * 8.0 / (best * 1e-3);
   return UT_OK;
 }
+int ut_debug_set_profile(int device, uint64_t* out, int reset) {
+  UT_CUDA(cudaSetDevice(device));
+#ifdef UT_SET_PROFILE
+  UT_CUDA(cudaDeviceSynchronize());
+  UT_CUDA(cudaMemcpyFromSymbol(out, g_setprof, sizeof(uint64_t) * kSetProfSlots));
+  if (reset) {
+    static const unsigned long long zero[kSetProfSlots] = {};
+    UT_CUDA(cudaMemcpyToSymbol(g_setprof, zero, sizeof(zero)));
+  }
+#else
+  for (int k = 0; k < kSetProfSlots; ++k) out[k] = 0;
+  (void)reset;
+#endif
+  return UT_OK;
+}
 int ut_debug_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t dd, int device, uint64_t* out) {
   UT_CUDA(cudaSetDevice(device));
   uint64_t* d = nullptr;

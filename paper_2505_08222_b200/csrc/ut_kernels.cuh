@@ -32,6 +32,7 @@ constexpr int kMeasStride = 8;    // ox, oy, r2, sigma, -1/(2 sigma^2) (+pad)
 constexpr int kMaxEntities = 64;  // spawn scratch per thread
 constexpr double kMergeFloor = 0x1p-860;  // see the merged-update argument in step_set
 constexpr int kChunkFlagDone = 1, kChunkFlagSpawned = 2;
+constexpr int kBcStatUpdates = 8, kBcStatResamples = 9, kBcStatExact = 10;  // Smem::bc slots
 
 // Strided view of one env's record: word w at p[w * n_envs].
 struct Rec {
@@ -57,7 +58,7 @@ struct Smem {
   double* tab_exp;   // [32]
   DevConfig* cfg;    // config of the env being filtered
   double* red;       // kRedDoubles: BlockReducer buffers + scan warp sums
-  double* bc;        // 16 broadcast slots
+  double* bc;        // 16 broadcast slots (0: resample draw; kBcStat*: the env's filter statistics)
   uint4* xch;        // [32 warps][5] lane-0 Philox blocks (misaligned streams)
   double* meas;      // [sA*sT][kMeasStride] pings of the env being filtered
   uint16_t* mcount;  // [sA*sT] measurements applied to each set this step
@@ -65,6 +66,7 @@ struct Smem {
   double* trk;       // [sA*sT][kTrkStride] the sets' track scalars + PF stream keys
   uint8_t* flags;    // [blockDim] per-env chunk flags
   uint64_t* mbar;    // TMA completion barrier
+  uint32_t mbar_sa, pf_sa;  // their shared-window addresses (computed once)
   double* pf;        // [5][P] TMA-prefetched next particle set
   double* cum;       // [P] resample scan | re-init words
   double* st;        // [4P] resample staging
@@ -115,6 +117,8 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int sA, int sT) {
   S.bc = F.bc;
   S.xch = F.xch;
   S.mbar = F.mbar;
+  S.mbar_sa = smem_addr(F.mbar);
+  S.pf_sa = smem_addr(F.pf);
   S.pf = F.pf;
   S.st = F.pf;
   S.cum = F.pf + 4 * NP;
@@ -839,17 +843,33 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   // the set buffer is next written by the prefetch after this set's estimate barrier
 }
 
+// Per-phase cycle profile of the particle-set loop (debug builds with
+// -DUT_SET_PROFILE only; thread 0 of each CTA, read by ut_debug_set_profile).
+constexpr int kSetProfSlots = 12;
+#ifdef UT_SET_PROFILE
+__shared__ long long g_sp_acc[kSetProfSlots + 1];
+__device__ unsigned long long g_setprof[kSetProfSlots];
+#define SETPROF(k)                                  \
+  if (threadIdx.x == 0) {                           \
+    const long long _n = clock64();                 \
+    g_sp_acc[k] += _n - g_sp_acc[kSetProfSlots];    \
+    g_sp_acc[kSetProfSlots] = _n;                   \
+  }
+#else
+#define SETPROF(k)
+#endif
+
 // Issue the TMA prefetch of particle set g (5 fields x P doubles) into S.pf.
 __device__ __forceinline__ void prefetch_set(const DevBatch& B, const Smem& S, int64_t g, int P) {
   const uint32_t bytes = (uint32_t)(sizeof(double) * P);
   const size_t off = (size_t)g * P;
   fence_proxy_async();
-  mbar_expect_tx(S.mbar, 5u * bytes);
-  bulk_g2s(S.pf, B.px + off, bytes, S.mbar);
-  bulk_g2s(S.pf + P, B.py + off, bytes, S.mbar);
-  bulk_g2s(S.pf + 2 * P, B.vx + off, bytes, S.mbar);
-  bulk_g2s(S.pf + 3 * P, B.vy + off, bytes, S.mbar);
-  bulk_g2s(S.pf + 4 * P, B.w + off, bytes, S.mbar);
+  mbar_expect_tx_sa(S.mbar_sa, 5u * bytes);
+  bulk_g2s_sa(S.pf_sa, B.px + off, bytes, S.mbar_sa);
+  bulk_g2s_sa(S.pf_sa + bytes, B.py + off, bytes, S.mbar_sa);
+  bulk_g2s_sa(S.pf_sa + 2 * bytes, B.vx + off, bytes, S.mbar_sa);
+  bulk_g2s_sa(S.pf_sa + 3 * bytes, B.vy + off, bytes, S.mbar_sa);
+  bulk_g2s_sa(S.pf_sa + 4 * bytes, B.w + off, bytes, S.mbar_sa);
 }
 
 // filter_step (env.cpp:349-363) + fused comm updates (env.cpp:385-392) +
@@ -977,7 +997,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     }
   }
   if (FULL) {
-    mbar_wait(S.mbar, tphase);
+    SETPROF(0);
+    mbar_wait_sa(S.mbar_sa, tphase);
+    SETPROF(1);
     tphase ^= 1u;
 #pragma unroll
     for (int q = 0; q < PPT; q += 2) {
@@ -1016,6 +1038,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   }
 
   // ---- range updates: own ping, then fused senders (env.cpp:356-360, 385-392)
+  SETPROF(2);
   const int nm = S.mcount[ti];
   const uint16_t* ml = S.mlist + ti * c.sA;
   bool have_ess = false;
@@ -1068,6 +1091,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       stage(j + 1);
     }
     if (nm & 1) stage(nm - 1);
+    SETPROF(3);
     __syncthreads();
     double shift = 0.0;  // sum_j s'_j, in stage order
 #pragma unroll 1
@@ -1099,7 +1123,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           lx = max(lx, __double2hiint(e[q]) >> 20);
         }
       }
+      SETPROF(4);
       const double2 r = R.sum2_imax<NW>(ls, lq, lx);
+      SETPROF(5);
       if (isfinite(r.x) && r.x > 0.0 && lx >= 1023 - 860) {  // max(e) >= 2^-860
         const double rcp = 1.0 / r.x;
 #pragma unroll
@@ -1113,10 +1139,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         exact = true;
       }
     }
-    if (exact && tid == 0) {
-      const Rec rec = rec_of(B, e);
-      STAT(9) += 1.0;
-    }
+    if (exact && tid == 0) S.bc[kBcStatExact] += 1.0;
   }
   if (exact && nm > 0) {
     __syncthreads();  // every thread holds its particles: S.pf becomes the staging area
@@ -1140,6 +1163,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // weights are the ones last step's maybe_resample already vetted (ESS >= P/2),
   // so the reference's recomputation cannot resample: skipped unless the state
   // was injected.
+  SETPROF(6);
   bool resampled = false;
   const bool ess_known_ok = nm == 0 && tk[TK_ESSOK] != 0.0;
   if (!ess_known_ok) {
@@ -1154,6 +1178,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
       const double u0 = (double)(((u0_hi << 32) | u0_lo) >> 11) * 0x1.0p-53;
       pf_resample<PPT, FULL, NW>(s, k0, P, u0, S);
+      SETPROF(7);
       resampled = true;
     }
   }
@@ -1163,13 +1188,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
            (long long)e, ps, nm, (int)exact, (int)have_ess, ess, (int)resampled,
            (unsigned long long)pos);  // at set start
 
-  // ---- estimate (env.cpp:403-407)
-  // The set buffer is free once every thread is past the estimate barrier: the
-  // next set of this chunk is prefetched into it then (generic-proxy writes to
-  // it are fenced against the async-proxy copy first).
-  if (FULL) fence_proxy_async();
-  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R);
-  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
+  // ---- the set back to HBM (before the estimate's reduction, whose latency
+  // then covers the stores' register reads)
   const size_t base = (size_t)gset * P;
   if (FULL) {
 #pragma unroll
@@ -1193,6 +1213,15 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       }
     }
   }
+  // ---- estimate (env.cpp:403-407)
+  // The set buffer is free once every thread is past the estimate barrier: the
+  // next set of this chunk is prefetched into it then (generic-proxy writes to
+  // it are fenced against the async-proxy copy first).
+  if (FULL) fence_proxy_async();
+  SETPROF(8);
+  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R);
+  SETPROF(9);
+  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
   if (tid == 0) {
     const Rec rec = rec_of(B, e);
     TRK(K_EX, ti) = est.x;
@@ -1203,9 +1232,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     // stream position: 4P predict draws, 2 for a resample (tracking.cpp:24-37, 160)
     TRK(K_POS, ti) = tk[TK_POS] + (noise ? 4.0 * (double)P : 0.0) + (resampled ? 2.0 : 0.0);
     TRK(K_ESSOK, ti) = 1.0;  // maybe_resample ran: ESS >= P/2 or weights uniform
-    STAT(7) += (double)nm;
-    STAT(8) += resampled ? 1.0 : 0.0;
+    S.bc[kBcStatUpdates] += (double)nm;
+    S.bc[kBcStatResamples] += resampled ? 1.0 : 0.0;
   }
+  SETPROF(10);
 }
 
 // Stage env e's config and ping schedule for the particle phase: measurement
@@ -1220,6 +1250,7 @@ __device__ __forceinline__ void stage_env(const DevConfig& cg, const DevBatch& B
   const uint8_t* link = present + sA * sT;
   for (int i = threadIdx.x; i < (int)(sizeof(DevConfig) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(S.cfg)[i] = reinterpret_cast<const uint32_t*>(&cg)[i];
+  if (threadIdx.x == 0) S.bc[kBcStatUpdates] = S.bc[kBcStatResamples] = S.bc[kBcStatExact] = 0.0;
   for (int i = threadIdx.x; i < A * T; i += blockDim.x) {
     const int a = i / T, t = i - (i / T) * T, ti = a * sT + t;
     double* m = S.meas + kMeasStride * ti;
@@ -1360,6 +1391,10 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
   const int set_end = (int)(hi < B.n_envs ? set_off(B, hi) : set_off(B, hi - 1) + cfg_of(B, hi - 1).A * cfg_of(B, hi - 1).T);
   __syncthreads();
   uint32_t tphase = 0;
+#ifdef UT_SET_PROFILE
+  if (threadIdx.x == 0)
+    for (int k = 0; k <= kSetProfSlots; ++k) g_sp_acc[k] = k == kSetProfSlots ? clock64() : 0;
+#endif
   // phase timing (thread 0, shared memory: nothing live in registers)
   __shared__ long long ph_cyc[kPhaseCount + 1];
   const bool timing = B.phase_cycles != nullptr;
@@ -1400,6 +1435,13 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
                                                            g + 1 < chunk_end ? g + 1 : -1);
         }
       __syncthreads();  // S.cfg / meas / mlist reused by the next env
+      if (threadIdx.x == 0) {  // the env's filter statistics, accumulated in smem per set
+        const DevConfig& cg = cfg_of(B, e);
+        double* st = B.rec + e + (int64_t)cg.o_stats * B.n_envs;
+        st[7 * B.n_envs] += S.bc[kBcStatUpdates];
+        st[8 * B.n_envs] += S.bc[kBcStatResamples];
+        st[9 * B.n_envs] += S.bc[kBcStatExact];
+      }
     }
     mark(PH_FILTER);
     // ---- 3. reward / done / info, one env per thread; then tokens
@@ -1434,6 +1476,10 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
   }
   if (timing && threadIdx.x == 0)
     for (int k = 0; k < kPhaseCount; ++k) B.phase_cycles[blockIdx.x * kPhaseCount + k] += (unsigned long long)ph_cyc[k];
+#ifdef UT_SET_PROFILE
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kSetProfSlots; ++k) atomicAdd(&g_setprof[k], (unsigned long long)g_sp_acc[k]);
+#endif
 }
 
 // Environment ctor / reset (env.cpp:110-151, 153-233) for every env. When
