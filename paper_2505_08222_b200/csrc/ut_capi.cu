@@ -108,8 +108,11 @@ DevConfig to_dev(const ut_env_config& c, int sA, int sT) {
   return d;
 }
 
-constexpr int kPPT = 4;
-constexpr int kMaxParticles = 1024;  // 256 threads x 4 particles per CTA
+#ifndef UT_PPT
+#define UT_PPT 4
+#endif
+constexpr int kPPT = UT_PPT;          // particles per thread
+constexpr int kMaxParticles = 1024;  // 1024 / kPPT threads x kPPT particles per CTA
 
 int threads_for(int P) {
   int nt = (P + kPPT - 1) / kPPT;

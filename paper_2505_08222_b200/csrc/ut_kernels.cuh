@@ -760,8 +760,11 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   double excl = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) excl = 0.0;
   if (lane == 31) wsum[warp] = incl;
-  static_assert(PPT == 4, "mark zeroing assumes 4 particles per thread");
-  if (FULL || k0 < P) *reinterpret_cast<int4*>(mark + k0) = make_int4(0, 0, 0, 0);
+  static_assert(PPT % 4 == 0, "mark zeroing takes whole int4s");
+  if (FULL || k0 < P) {
+#pragma unroll
+    for (int i = 0; i < PPT; i += 4) *reinterpret_cast<int4*>(mark + k0 + i) = make_int4(0, 0, 0, 0);
+  }
   __syncthreads();
   double woff = 0.0;  // cum[k] = (sum of earlier warps' totals + excl) + loc[q]
   if constexpr (NW > 0) {
@@ -803,12 +806,13 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   }
   __syncthreads();
   int r[PPT];
-  {
-    const int4 m4 = (FULL || k0 < P) ? *reinterpret_cast<const int4*>(mark + k0) : make_int4(0, 0, 0, 0);
-    r[0] = m4.x;
-    r[1] = max(m4.y, r[0]);
-    r[2] = max(m4.z, r[1]);
-    r[3] = max(m4.w, r[2]);
+#pragma unroll
+  for (int i = 0; i < PPT; i += 4) {
+    const int4 m4 = (FULL || k0 < P) ? *reinterpret_cast<const int4*>(mark + k0 + i) : make_int4(0, 0, 0, 0);
+    r[i] = i == 0 ? m4.x : max(m4.x, r[i - 1]);
+    r[i + 1] = max(m4.y, r[i]);
+    r[i + 2] = max(m4.z, r[i + 1]);
+    r[i + 3] = max(m4.w, r[i + 2]);
   }
   int mi = r[PPT - 1];
 #pragma unroll
@@ -915,22 +919,30 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 
   // ---- Philox words of fill_normals (tracking.cpp:24-37): particle k needs the
   // words at pos + s*P + k for segments s = 0..3. FULL: thread t computes the
-  // aligned block (pos/4 + s*P/4 + t) of each segment; a misaligned stream takes
-  // its remaining words from the next lane's block (shuffle). Lane 31 needs the
-  // block after its warp's range in each segment: lanes 0..3 of every warp
-  // compute those four as a fifth, interleaved chain (so no warp waits for
-  // another) and hand them over through the warp's xch slots. The last warp's
-  // segment-3 extra block, pos/4 + P, also holds the resample draw at pos + 4P.
-  uint4 blk[4];
+  // NB = PPT/4 aligned blocks pos/4 + s*P/4 + NB*t + i of each segment; a
+  // misaligned stream takes its remaining words from the next lane's first
+  // block (shuffle). Lane 31 needs the block after its warp's range in each
+  // segment: lanes 0..3 of every warp compute those four as one more,
+  // interleaved chain (so no warp waits for another) and hand them over through
+  // the warp's xch slots. The last warp's segment-3 extra block, pos/4 + P, also
+  // holds the resample draw at pos + 4P.
+  constexpr int NB = PPT / 4 > 0 ? PPT / 4 : 1;
+  uint4 blk[4][NB];
   if (FULL && noise) {
-    const uint64_t b0 = (pos >> 2) + (uint64_t)tid;
-    const uint64_t bq[5] = {b0, b0 + (uint64_t)(P / 4), b0 + 2 * (uint64_t)(P / 4), b0 + 3 * (uint64_t)(P / 4),
-                            (pos >> 2) + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + (uint64_t)(32 * (warp + 1))};
-    uint4 bo[5];
-    philox_n<5>(key, (uint64_t)ps, bq, bo);
+    uint64_t bq[4 * NB + 1];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) blk[q] = bo[q];
-    const uint4 ex = bo[4];
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        bq[q * NB + i] = (pos >> 2) + (uint64_t)q * (uint64_t)(P / 4) + (uint64_t)(NB * tid + i);
+    bq[4 * NB] = (pos >> 2) + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + (uint64_t)(NB * 32 * (warp + 1));
+    uint4 bo[4 * NB + 1];
+    philox_n<4 * NB + 1>(key, (uint64_t)ps, bq, bo);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int i = 0; i < NB; ++i) blk[q][i] = bo[q * NB + i];
+    const uint4 ex = bo[4 * NB];
     if (lane < 4) S.xch[warp * 5 + lane] = ex;
     if (warp == nw - 1 && lane == 3) {
       const uint4 y = off == 3 ? philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P + 1) : ex;
@@ -957,16 +969,29 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   if (noise) {
     uint32_t W[4][PPT];  // [segment][particle]
     if (FULL) {
-      if constexpr (PPT == 4) {
+      static_assert(PPT % 4 == 0, "the FULL path takes whole Philox blocks");
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 nb;
-          nb.x = __shfl_down_sync(0xffffffffu, blk[q].x, 1);
-          nb.y = __shfl_down_sync(0xffffffffu, blk[q].y, 1);
-          nb.z = __shfl_down_sync(0xffffffffu, blk[q].z, 1);
-          if (off != 0 && lane == 31) nb = S.xch[warp * 5 + q];
-          words_at(blk[q], nb, off, W[q]);
+      for (int q = 0; q < 4; ++q) {
+        // this thread's window: its NB blocks, then the next lane's first block
+        uint4 nb;
+        nb.x = __shfl_down_sync(0xffffffffu, blk[q][0].x, 1);
+        nb.y = __shfl_down_sync(0xffffffffu, blk[q][0].y, 1);
+        nb.z = __shfl_down_sync(0xffffffffu, blk[q][0].z, 1);
+        if (off != 0 && lane == 31) nb = S.xch[warp * 5 + q];
+        uint32_t a[4 * NB + 3];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          a[4 * i] = blk[q][i].x, a[4 * i + 1] = blk[q][i].y, a[4 * i + 2] = blk[q][i].z, a[4 * i + 3] = blk[q][i].w;
         }
+        a[4 * NB] = nb.x, a[4 * NB + 1] = nb.y, a[4 * NB + 2] = nb.z;
+        // word j of the window starting at `off` (branch-free: a 2-word, then a
+        // 1-word shift)
+        const bool s2 = off & 2, s1 = off & 1;
+        uint32_t b[PPT + 1];
+#pragma unroll
+        for (int j = 0; j <= PPT; ++j) b[j] = s2 ? a[j + 2] : a[j];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) W[q][j] = s1 ? b[j + 1] : b[j];
       }
     } else {
 #pragma unroll
@@ -1374,7 +1399,7 @@ __device__ __noinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t
 
 // The fused step.
 template <int PPT, int NP, bool FULL>
-__global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode, int32_t* status) {
+__global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem S = carve<NP>(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT);
   const DevBatch& Bg = *B.self;  // cold paths read the global copy
@@ -1486,7 +1511,7 @@ __global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch 
 // `ctor` is set the record starts zeroed and each set's stream is advanced past
 // pf::init's 8P draws (tracking.cpp:43-67), whose values spawn overwrites.
 template <int PPT, int NP>
-__global__ void __launch_bounds__(256, UT_STEP_MIN_BLOCKS) reset_kernel(DevBatch B, int ctor, int32_t* status) {
+__global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) reset_kernel(DevBatch B, int ctor, int32_t* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem S = carve<NP>(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT);
   const DevBatch& Bg = *B.self;
