@@ -814,16 +814,20 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
     r[i + 2] = max(m4.z, r[i + 1]);
     r[i + 3] = max(m4.w, r[i + 2]);
   }
-  int mi = r[PPT - 1];
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, mi, o);
-    if (lane >= o) mi = max(mi, y);
-  }
-  int mex = __shfl_up_sync(0xffffffffu, mi, 1);
-  if (lane == 0) mex = -1;
+  // Across lanes: the marks are increasing wherever they are set (counts grow
+  // with the particle index), so the prefix max before a lane is the value of
+  // the nearest lower lane holding a mark -- one ballot and one shuffle instead
+  // of a five-level max scan.
+  const int mi = r[PPT - 1];
+  const unsigned nz = __ballot_sync(0xffffffffu, mi != 0);
+  const unsigned below = nz & ((1u << lane) - 1u);
+  const int src = below ? 31 - __clz(below) : lane;
+  const int top = nz ? 31 - __clz(nz) : 0;
+  int mex = __shfl_sync(0xffffffffu, mi, src);
+  const int wtop = __shfl_sync(0xffffffffu, mi, top);
+  if (!below) mex = -1;
   int* wmx = reinterpret_cast<int*>(wsum + 96);
-  if (lane == 31) wmx[warp] = mi;
+  if (lane == 31) wmx[warp] = wtop;
   __syncthreads();
   if constexpr (NW > 0) {
 #pragma unroll
