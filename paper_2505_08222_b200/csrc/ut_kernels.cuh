@@ -1060,7 +1060,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       const double sp = sqrt_rn_clamp(s.vx[j] * s.vx[j] + s.vy[j] * s.vy[j]);
-      const double f = sp > ms ? div_rn_clamp(ms, sp) : 1.0;
+      // branch-free: the quotient is formed for every particle (sp = 0 gives
+      // inf/NaN, discarded by the select)
+      const double qt = div_rn_clamp(ms, sp);
+      const double f = sp > ms ? qt : 1.0;
       s.vx[j] = s.vx[j] * f;
       s.vy[j] = s.vy[j] * f;
     }
