@@ -1094,7 +1094,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     float* mb = reinterpret_cast<float*>(R.buf());  // per-stage warp maxima, [stage * 32 + warp]
     // one stage: every particle's log-likelihood for measurement j, added to L in
     // stage order, and the stage's warp maximum (rounded up to fp32)
-    auto stage = [&](int j) {
+    auto stage = [&](int j) -> float {
       const double* m = S.meas + kMeasStride * ml[j];
       const double ox = m[0], oy = m[1], r2 = m[2], c2 = m[4];
       float mj = -CUDART_INF_F;
@@ -1109,20 +1109,27 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           mj = fmaxf(mj, __double2float_ru(ll));
         }
       }
-      // warp max through an order-preserving int key (one REDUX instead of 5 shuffles)
+      return mj;
+    };
+    // warp max of a stage through an order-preserving int key (one REDUX
+    // instead of 5 shuffles)
+    auto stage_max = [&](int j, float mj) {
       int key = __float_as_int(mj);
       key ^= (key >> 31) & 0x7fffffff;
       key = __reduce_max_sync(0xffffffffu, key);
       key ^= (key >> 31) & 0x7fffffff;
       if (lane == 0) mb[j * 32 + warp] = __int_as_float(key);
     };
-    // two stages per iteration so their distance / sqrt chains interleave
+    // two stages per iteration so their distance / sqrt chains interleave (the
+    // warp reductions, whose divergence check fences the scheduler, follow both)
 #pragma unroll 1
     for (int j = 0; j + 1 < nm; j += 2) {
-      stage(j);
-      stage(j + 1);
+      const float m0 = stage(j);
+      const float m1 = stage(j + 1);
+      stage_max(j, m0);
+      stage_max(j + 1, m1);
     }
-    if (nm & 1) stage(nm - 1);
+    if (nm & 1) stage_max(nm - 1, stage(nm - 1));
     SETPROF(3);
     __syncthreads();
     double shift = 0.0;  // sum_j s'_j, in stage order
