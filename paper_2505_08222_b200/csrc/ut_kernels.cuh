@@ -696,18 +696,34 @@ __device__ __noinline__ int pf_update_seq(const double* m, int k0, int P, const 
 // more than ~1e-11 relative.
 template <int PPT, bool FULL, int NW>
 __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, int P, double cx, double cy,
-                                               BlockReducer& R) {
+                                               BlockReducer& R, bool uniform = false) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  if (uniform) {  // weights all 1/n (just resampled): plain moments, scaled once
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    if (FULL || k0 + j < P) {
-      const double dx = s.px[j] - cx, dy = s.py[j] - cy;
-      a0 = a0 + s.w[j] * dx;
-      a1 = a1 + s.w[j] * dy;
-      a2 = a2 + s.w[j] * (dx * dx + dy * dy);
+    for (int j = 0; j < PPT; ++j) {
+      if (FULL || k0 + j < P) {
+        const double dx = s.px[j] - cx, dy = s.py[j] - cy;
+        a0 = a0 + dx;
+        a1 = a1 + dy;
+        a2 = a2 + (dx * dx + dy * dy);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      if (FULL || k0 + j < P) {
+        const double dx = s.px[j] - cx, dy = s.py[j] - cy;
+        a0 = a0 + s.w[j] * dx;
+        a1 = a1 + s.w[j] * dy;
+        a2 = a2 + s.w[j] * (dx * dx + dy * dy);
+      }
     }
   }
-  const double3 m = R.sum3<NW>(a0, a1, a2);
+  double3 m = R.sum3<NW>(a0, a1, a2);
+  if (uniform) {
+    const double inv = 1.0 / (double)P;
+    m.x = m.x * inv, m.y = m.y * inv, m.z = m.z * inv;
+  }
   const double mx = cx + m.x, my = cy + m.y;
   const double shift2 = m.x * m.x + m.y * m.y;
   const double var = m.z - shift2;
@@ -734,18 +750,18 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   double* wsum = S.red + 2 * kRedSlots;  // [32] warp totals, then [32] int warp maxima at +96
   // Staging layout: particle k = k0 + q of thread t at q * NT + t, so each
   // field's stores are lane-contiguous (conflict-free); a field spans FS slots.
+  // Positions and velocities are staged as pairs, one 128-bit access each.
   const int NT = NW > 0 ? NW * 32 : (int)blockDim.x;
   const int FS = NT * PPT;
+  double2* st2 = reinterpret_cast<double2*>(st);  // [FS] (px, py), then [FS] (vx, vy)
   double loc[PPT];
   double run = 0.0;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     const int k = k0 + q;
     if (FULL || k < P) {
-      st[q * NT + tid] = s.px[q];
-      st[FS + q * NT + tid] = s.py[q];
-      st[2 * FS + q * NT + tid] = s.vx[q];
-      st[3 * FS + q * NT + tid] = s.vy[q];
+      st2[q * NT + tid] = make_double2(s.px[q], s.py[q]);
+      st2[FS + q * NT + tid] = make_double2(s.vx[q], s.vy[q]);
       run = q == 0 ? s.w[q] : run + s.w[q];
     }
     loc[q] = run;
@@ -841,10 +857,9 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
     if (FULL || k0 + q < P) {
       const int i = max(mex, r[q]);
       const int j = (i & (PPT - 1)) * NT + i / PPT;
-      s.px[q] = st[j];
-      s.py[q] = st[FS + j];
-      s.vx[q] = st[2 * FS + j];
-      s.vy[q] = st[3 * FS + j];
+      const double2 p2 = st2[j], v2 = st2[FS + j];
+      s.px[q] = p2.x, s.py[q] = p2.y;
+      s.vx[q] = v2.x, s.vy[q] = v2.y;
       s.w[q] = inv_n;
     }
   }
@@ -1258,7 +1273,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // it are fenced against the async-proxy copy first).
   if (FULL) fence_proxy_async();
   SETPROF(8);
-  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R);
+  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R, resampled);
   SETPROF(9);
   if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
   if (tid == 0) {
