@@ -24,6 +24,10 @@ struct ut_vecenv;
  * sequential update path (tracking.cpp:119-143 once per measurement) instead of
  * the merged one; trace_env >= 0 printf's a per-set trace for that env. */
 int ut_debug_set_knobs(struct ut_vecenv* v, int force_exact, int64_t trace_env);
+/* Per-CTA cycle totals of the step kernel since phase timing was enabled
+ * (ut_vecenv_enable_phase_timing): *n = grid size; out may be NULL to query it.
+ * Shows the load balance of the persistent grid. */
+int ut_debug_cta_cycles(struct ut_vecenv* v, uint64_t* out, int64_t cap, int64_t* n);
 /* sizeof of the ABI structs as compiled: ut_env_config, ut_buffers,
  * ut_host_outputs, ut_benchmark_report (no device needed). */
 int ut_debug_abi_sizes(int64_t out[4]);

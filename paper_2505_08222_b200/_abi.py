@@ -146,6 +146,8 @@ def declare_debug(lib):
     lib.ut_debug_derive_key.restype = C.c_int
     lib.ut_debug_fp64_peak.argtypes = [C.c_int, C.POINTER(C.c_double)]
     lib.ut_debug_fp64_peak.restype = C.c_int
+    lib.ut_debug_cta_cycles.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64)]
+    lib.ut_debug_cta_cycles.restype = C.c_int
     lib.ut_debug_abi_sizes.argtypes = [C.POINTER(C.c_int64)]
     lib.ut_debug_abi_sizes.restype = C.c_int
     lib.ut_debug_ieee_check.argtypes = [C.c_int, C.c_uint64, C.c_int64, C.c_int, C.POINTER(C.c_uint64)]

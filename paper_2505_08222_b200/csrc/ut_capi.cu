@@ -1151,6 +1151,20 @@ int ut_debug_set_knobs(ut_vecenv* v, int force_exact, int64_t trace_env) {
   v->B.trace_env = trace_env;
   return v->sync_batch();
 }
+int ut_debug_cta_cycles(ut_vecenv* v, uint64_t* out, int64_t cap, int64_t* n) {
+  *n = v->phase_buf ? (int64_t)v->grid : 0;
+  if (!v->phase_buf || !out) return UT_OK;
+  if (cap < *n) return fail(UT_ERR_CONTRACT, "cta_cycles: room for %lld CTAs, need %lld", (long long)cap, (long long)*n);
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  std::vector<unsigned long long> h((size_t)v->grid * kPhaseCount);
+  UT_CUDA(cudaMemcpy(h.data(), v->phase_buf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+  for (int64_t b = 0; b < *n; ++b) {
+    uint64_t t = 0;
+    for (int k = 0; k < kPhaseCount; ++k) t += h[(size_t)b * kPhaseCount + k];
+    out[b] = t;
+  }
+  return UT_OK;
+}
 int ut_debug_abi_sizes(int64_t out[4]) {
   out[0] = sizeof(ut_env_config);
   out[1] = sizeof(ut_buffers);
