@@ -252,14 +252,27 @@ struct ut_vecenv {
     } else if ((rc = wait_outputs(cur))) {
       return rc;
     }
+    void (*kern)(DevBatch, int, int32_t*) = nullptr;
     if (full && np == 1024)
-      step_kernel<kPPT, 1024, true><<<g, b, smem, stream>>>(B, mode, d_status);
+      kern = step_kernel<kPPT, 1024, true>;
     else if (full && np == 512)
-      step_kernel<kPPT, 512, true><<<g, b, smem, stream>>>(B, mode, d_status);
+      kern = step_kernel<kPPT, 512, true>;
     else if (full && np == 256)
-      step_kernel<kPPT, 256, true><<<g, b, smem, stream>>>(B, mode, d_status);
+      kern = step_kernel<kPPT, 256, true>;
     else
-      step_kernel<kPPT, 1024, false><<<g, b, smem, stream>>>(B, mode, d_status);
+      kern = step_kernel<kPPT, 1024, false>;
+    // cooperative: the kernel's phases are separated by grid-wide barriers
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = g;
+    lc.blockDim = b;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    UT_CUDA(cudaLaunchKernelEx(&lc, kern, B, mode, d_status));
     ++launches;
     UT_CUDA(cudaGetLastError());
     return UT_OK;
@@ -424,6 +437,8 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   // debug knob (occupancy experiments): cap resident CTAs per SM
   if (const char* cap = getenv("UT_DEBUG_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(cap)));
   v->grid = (int)std::min<int64_t>(n_envs, (int64_t)per_sm * sms);
+  if ((rc = v->alloc(&B.work, 1))) return rc;
+  UT_CUDA(cudaMemsetAsync(B.work, 0, sizeof(int), v->stream));
   if ((rc = v->alloc(&v->d_self, 1))) return rc;
   if ((rc = v->sync_batch())) return rc;
 

@@ -21,9 +21,12 @@
 //   4. RESET     finished envs: spawn (one env per thread) + particle re-init
 //      (whole CTA per set) + fresh tokens.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "ut_device.cuh"
 
 namespace ut {
+namespace cg = cooperative_groups;
 
 enum StepMode : int { MODE_EXTERNAL = -1, MODE_RANDOM = 0, MODE_SCRIPTED = 1 };
 enum DevStatus : int { ST_OK = 0, ST_SPAWN_INFEASIBLE = 2 };
@@ -33,6 +36,7 @@ constexpr int kMaxEntities = 64;  // spawn scratch per thread
 constexpr double kMergeFloor = 0x1p-860;  // see the merged-update argument in step_set
 constexpr int kChunkFlagDone = 1, kChunkFlagSpawned = 2;
 constexpr int kBcStatUpdates = 8, kBcStatResamples = 9, kBcStatExact = 10;  // Smem::bc slots
+constexpr int kBcClaim = 11;  // the filter phase's next env (int)
 
 // Strided view of one env's record: word w at p[w * n_envs].
 struct Rec {
@@ -1442,7 +1446,6 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     cta_range(B.n_envs, lo64, hi64);
     lo = (int)lo64, hi = (int)hi64;
   }
-  const int set_end = (int)(hi < B.n_envs ? set_off(B, hi) : set_off(B, hi - 1) + cfg_of(B, hi - 1).A * cfg_of(B, hi - 1).T);
   __syncthreads();
   uint32_t tphase = 0;
 #ifdef UT_SET_PROFILE
@@ -1461,43 +1464,61 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
       ph_cyc[kPhaseCount] = now;
     }
   };
+  // Three phases separated by grid-wide barriers (cooperative launch: every CTA
+  // is resident): the env prologues of the CTA's static env range; the particle
+  // filters, envs handed out one at a time by a global counter so the grid
+  // finishes together (a static split left the slowest CTA 5 % behind the
+  // mean); then outputs and auto-resets of the static range.
+  cg::grid_group grid = cg::this_grid();
+  const int n = (int)B.n_envs;
+  mark(-1);
+  // ---- 1. prologue, one env per thread
+  for (int e0 = lo; e0 < hi; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    if (e < min(hi, e0 + (int)blockDim.x)) env_prologue(cfg_of(Bg, e), Bg, e, B.env_index_offset + e, mode);
+  }
+  mark(PH_PROLOGUE);
+  grid.sync();  // every env's ping schedule is in place
+  // ---- 2. particle sets, env by env from the work counter; the next env is
+  // claimed at the start of the current one so its first set can be prefetched
+  int* claim = reinterpret_cast<int*>(S.bc + kBcClaim);
+  if (threadIdx.x == 0) {
+    const int e = atomicAdd(B.work, 1);
+    *claim = e;
+    if (FULL && e < n) prefetch_set(B, S, set_off(B, e), B.P);
+  }
+  __syncthreads();
+  int e = *claim;
+  while (e < n) {
+    stage_env(cfg_of(B, e), B, S, rec_of(B, e), e);
+    if (threadIdx.x == 0) *claim = atomicAdd(B.work, 1);
+    __syncthreads();
+    const int en = *claim;
+    const DevConfig& c = *S.cfg;
+    const int so = (int)set_off(B, e);
+    const int nA = c.A, nT = c.T;
+    const int first_next = en < n ? (int)set_off(B, en) : -1;
+    for (int a = 0; a < nA; ++a)
+      for (int t = 0; t < nT; ++t) {
+        const int g = so + a * nT + t;
+        const int last = a == nA - 1 && t == nT - 1;
+        step_set<PPT, FULL, FULL ? NP / (32 * PPT) : 0>(c, B, S, R, e, g, a, t, tphase, last ? first_next : g + 1);
+      }
+    __syncthreads();  // S.cfg / meas / mlist / claim reused by the next env
+    if (threadIdx.x == 0) {  // the env's filter statistics, accumulated in smem per set
+      const DevConfig& cg = cfg_of(B, e);
+      double* st = B.rec + e + (int64_t)cg.o_stats * B.n_envs;
+      st[7 * B.n_envs] += S.bc[kBcStatUpdates];
+      st[8 * B.n_envs] += S.bc[kBcStatResamples];
+      st[9 * B.n_envs] += S.bc[kBcStatExact];
+    }
+    e = en;
+  }
+  mark(PH_FILTER);
+  grid.sync();  // every estimate is in place
+  if (blockIdx.x == 0 && threadIdx.x == 0) *B.work = 0;  // for the next launch
   for (int e0 = lo; e0 < hi; e0 += blockDim.x) {
     const int e1 = min(hi, e0 + (int)blockDim.x);
-    // the chunk's sets [set_off(e0), chunk_end) are prefetched one ahead; the
-    // set buffer is free at chunk boundaries (the reset phase uses it)
-    const int chunk_end = (int)(e1 < B.n_envs ? set_off(B, e1) : set_end);
-    if (FULL && threadIdx.x == 0) prefetch_set(B, S, set_off(B, e0), B.P);
-    mark(-1);
-    // ---- 1. prologue, one env per thread
-    {
-      const int e = e0 + threadIdx.x;
-      if (e < e1) env_prologue(cfg_of(Bg, e), Bg, e, B.env_index_offset + e, mode);
-    }
-    __syncthreads();
-    mark(PH_PROLOGUE);
-    // ---- 2. every particle set of the chunk
-    for (int e = e0; e < e1; ++e) {
-      stage_env(cfg_of(B, e), B, S, rec_of(B, e), e);
-      __syncthreads();
-      const DevConfig& c = *S.cfg;
-      const int so = (int)set_off(B, e);
-      const int nA = c.A, nT = c.T;
-      for (int a = 0; a < nA; ++a)
-        for (int t = 0; t < nT; ++t) {
-          const int g = so + a * nT + t;
-          step_set<PPT, FULL, FULL ? NP / (32 * PPT) : 0>(c, B, S, R, e, g, a, t, tphase,
-                                                           g + 1 < chunk_end ? g + 1 : -1);
-        }
-      __syncthreads();  // S.cfg / meas / mlist reused by the next env
-      if (threadIdx.x == 0) {  // the env's filter statistics, accumulated in smem per set
-        const DevConfig& cg = cfg_of(B, e);
-        double* st = B.rec + e + (int64_t)cg.o_stats * B.n_envs;
-        st[7 * B.n_envs] += S.bc[kBcStatUpdates];
-        st[8 * B.n_envs] += S.bc[kBcStatResamples];
-        st[9 * B.n_envs] += S.bc[kBcStatExact];
-      }
-    }
-    mark(PH_FILTER);
     // ---- 3. reward / done / info, one env per thread; then tokens
     {
       const int e = e0 + threadIdx.x;
@@ -1524,7 +1545,6 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
       write_outputs(Bg, e0, e1, S.flags, kChunkFlagSpawned, false);
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagSpawned)) B.step[e] = 0;
     }
-    if (FULL) fence_proxy_async();  // re-init words in the set buffer vs the next chunk's prefetch
     __syncthreads();
     mark(PH_RESET);
   }

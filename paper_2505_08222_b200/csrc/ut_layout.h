@@ -94,6 +94,7 @@ struct DevBatch {
   double* sched_r2;           // [n_envs][sA * sT] horizontal ranges this step
   uint8_t* sched_flags;       // [n_envs][sA * sT + sA * sA] ping present | link
   double *px, *py, *vx, *vy, *w;
+  int* work;  // the step kernel's env counter for the filter phase (0 between launches)
   // batch outputs
   int64_t obs_rows, global_rows;
   double* obs;
