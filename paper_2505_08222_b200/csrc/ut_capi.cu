@@ -430,7 +430,8 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   UT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)v->smem));
   UT_CUDA(cudaFuncSetAttribute((const void*)reset_kernel<kPPT, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)v->smem_reset));
-  // persistent grid: every resident CTA slot, each owning a contiguous env range
+  // persistent cooperative grid: every resident CTA slot (the step kernel's
+  // phases are separated by grid barriers, so all CTAs must be co-resident)
   int per_sm = 0;
   UT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v->nt, v->smem));
   if (per_sm < 1) return fail(UT_ERR_RUNTIME, "step kernel cannot be resident with %zu B shared memory", v->smem);

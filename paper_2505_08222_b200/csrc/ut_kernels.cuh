@@ -1,15 +1,17 @@
 // ut_kernels.cuh -- the fused environment-step kernel and its helpers.
 //
-// One persistent launch per step ("one fused kernel per step", north_star). Each
-// CTA owns a contiguous range of envs and walks it in chunks of blockDim.x envs:
+// One persistent, cooperative launch per step ("one fused kernel per step",
+// north_star), in phases separated by grid barriers. Phases 1, 3 and 4 walk the
+// CTA's contiguous env range in chunks of blockDim.x envs; phase 2 takes envs one
+// at a time from a global counter, so every CTA stays busy until the end:
 //
 //   1. PROLOGUE  one env per THREAD: actions, move_targets, move_agents,
 //      measure_ranges and the comm-drop decisions, in the reference's serial
 //      env-stream order, on that env's structure-of-arrays
 //      record (coalesced across the threads of the chunk). The ping schedule is
 //      handed to phase 2 through a small per-env scratch.
-//   2. FILTER    the whole CTA streams through every particle set of the chunk's
-//      envs (sets of consecutive envs are contiguous in HBM), each set held in
+//   2. FILTER    the whole CTA streams through every particle set of each env it
+//      claims (an env's sets are contiguous in HBM), each set held in
 //      registers -- PPT consecutive particles per thread, 128-bit loads/stores,
 //      read once and written once per step: predict (Philox words generated one
 //      set ahead, correctly rounded fp32 Box-Muller), ONE merged pass for all of
