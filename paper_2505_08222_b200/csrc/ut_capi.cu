@@ -100,6 +100,7 @@ DevConfig to_dev(const ut_env_config& c, int sA, int sT) {
   d.vn = c.pf.process_noise_vel;
   d.speed_margin = c.pf.speed_margin;
   d.init_radius = c.pf.init_radius;
+  d.inv_P = 1.0 / (double)c.pf.n_particles;
   d.head_a = c.heading_a;
   d.head_b = c.heading_b;
   d.head_noise = c.heading_noise_std;

@@ -702,7 +702,7 @@ __device__ __noinline__ int pf_update_seq(const double* m, int k0, int P, const 
 // more than ~1e-11 relative.
 template <int PPT, bool FULL, int NW>
 __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, int P, double cx, double cy,
-                                               BlockReducer& R, bool uniform = false) {
+                                               BlockReducer& R, bool uniform = false, double inv_n = 0.0) {
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   if (uniform) {  // weights all 1/n (just resampled): plain moments, scaled once
 #pragma unroll
@@ -726,14 +726,12 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
     }
   }
   double3 m = R.sum3<NW>(a0, a1, a2);
-  if (uniform) {
-    const double inv = 1.0 / (double)P;
-    m.x = m.x * inv, m.y = m.y * inv, m.z = m.z * inv;
-  }
+  if (uniform) m.x = m.x * inv_n, m.y = m.y * inv_n, m.z = m.z * inv_n;
   const double mx = cx + m.x, my = cy + m.y;
   const double shift2 = m.x * m.x + m.y * m.y;
   const double var = m.z - shift2;
-  if (var > 1e-5 * shift2) return make_double3(mx, my, sqrt(var));
+  // var > 0 here; far above 2^-960 for any spread a set can have
+  if (var > 1e-5 * shift2) return make_double3(mx, my, sqrt_rn_clamp(var));
   double acc = 0.0;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
@@ -749,7 +747,7 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
 // output j takes the first particle whose cumulative weight reaches (j + u0)/n,
 // clamped to n - 1 (the reference's monotone two-pointer walk).
 template <int PPT, bool FULL, int NW>
-__device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Smem& S) {
+__device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double inv_n, const Smem& S) {
   const int tid = threadIdx.x;
   int* mark = reinterpret_cast<int*>(S.cum);  // [P] source marks of the outputs
   double* st = S.st;
@@ -803,7 +801,6 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, const Sme
   // count(cum[k]) with k + 1 (the max wins where zero-weight particles share a
   // boundary) and a prefix max over the marks (0 where unmarked) hands every
   // output its source; outputs past count(cum[n-2]) fall to n - 1.
-  const double inv_n = 1.0 / (double)P;
   // count(c) = floor(c n - u0) + 1, clamped to [0, n]. It can differ from the
   // count against the rounded u_j = (j + u0)/n only when c n - u0 lies within
   // ~1e-13 of an integer; the block-tree cumulative weights already differ
@@ -1187,12 +1184,14 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       const double2 r = R.sum2_imax<NW>(ls, lq, lx);
       SETPROF(5);
       if (isfinite(r.x) && r.x > 0.0 && lx >= 1023 - 860) {  // max(e) >= 2^-860
-        const double rcp = 1.0 / r.x;
+        // r.x in [2^-860, P] and r.x^2, r.y >= 2^-400 where the ESS is formed:
+        // the branch-free IEEE divisions apply
+        const double rcp = div_rn_clamp(1.0, r.x);
 #pragma unroll
         for (int q = 0; q < PPT; ++q) s.w[q] = div_rcp(e[q], r.x, rcp);
         // ESS = sum^2 / sum(e^2) unless the squares may have underflowed
         if (lx >= 1023 - 200) {
-          ess = (r.x * r.x) / r.y;
+          ess = div_rn_clamp(r.x * r.x, r.y);
           have_ess = true;
         }
       } else {
@@ -1237,7 +1236,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       const uint64_t u0_lo = reinterpret_cast<const uint32_t*>(S.bc)[0];
       const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
       const double u0 = (double)(((u0_hi << 32) | u0_lo) >> 11) * 0x1.0p-53;
-      pf_resample<PPT, FULL, NW>(s, k0, P, u0, S);
+      pf_resample<PPT, FULL, NW>(s, k0, P, u0, c.inv_P, S);
       SETPROF(7);
       resampled = true;
     }
@@ -1248,8 +1247,16 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
            (long long)e, ps, nm, (int)exact, (int)have_ess, ess, (int)resampled,
            (unsigned long long)pos);  // at set start
 
-  // ---- the set back to HBM (before the estimate's reduction, whose latency
-  // then covers the stores' register reads)
+  // ---- estimate (env.cpp:403-407)
+  // The set buffer is free once every thread is past the estimate barrier: the
+  // next set of this chunk is prefetched into it then (generic-proxy writes to
+  // it are fenced against the async-proxy copy first).
+  if (FULL) fence_proxy_async();
+  SETPROF(8);
+  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R, resampled, c.inv_P);
+  SETPROF(9);
+  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
+  // ---- the set back to HBM
   const size_t base = (size_t)gset * P;
   if (FULL) {
     // 256-bit stores (STG.E.ENL2.256): one per field and 4 particles
@@ -1274,15 +1281,6 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       }
     }
   }
-  // ---- estimate (env.cpp:403-407)
-  // The set buffer is free once every thread is past the estimate barrier: the
-  // next set of this chunk is prefetched into it then (generic-proxy writes to
-  // it are fenced against the async-proxy copy first).
-  if (FULL) fence_proxy_async();
-  SETPROF(8);
-  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R, resampled);
-  SETPROF(9);
-  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
   if (tid == 0) {
     const Rec rec = rec_of(B, e);
     TRK(K_EX, ti) = est.x;

@@ -58,6 +58,7 @@ struct DevConfig {
   double eps_min, eps_max, d_min, d_safe;
   double min_sep, disc_r, pert_std, depth_min, depth_max;
   double pn, vn, speed_margin, init_radius;
+  double inv_P;  // RN(1 / P), the weight after a resample (tracking.cpp:149, 168)
   double head_a, head_b, head_noise, max_turn;
   // record layout (field-word offsets) for the batch strides sA >= A, sT >= T:
   // agent field f of agent a: o_agent + f sA + a; target: o_target + f sT + t;
