@@ -60,7 +60,7 @@ enum : int { TK_POS = 0, TK_MAXSPEED, TK_EX, TK_EY, TK_ESSOK, TK_AGE, TK_EVER, T
 
 struct Smem {
   double2* tab_log;  // [128]
-  double2* tab_sc;   // [64]
+  double2* tab_sc;   // [64][8] (replicated, see sincos_table)
   double* tab_exp;   // [32]
   DevConfig* cfg;    // config of the env being filtered
   double* red;       // kRedDoubles: BlockReducer buffers + scan warp sums
@@ -87,7 +87,7 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 template <int NP>
 struct FixedSmem {
   double2 tab_log[128];
-  double2 tab_sc[64];
+  double2 tab_sc[64 * 8];
   double tab_exp[32];
   double red[kRedDoubles];
   double bc[16];
@@ -156,7 +156,8 @@ __device__ __forceinline__ int64_t set_off(const DevBatch& B, int64_t e) {
 
 __device__ __forceinline__ void load_tables(const Smem& S) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) S.tab_log[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) S.tab_sc[i] = make_double2(kSinCosTab[2 * i], kSinCosTab[2 * i + 1]);
+  for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x)
+    S.tab_sc[i] = make_double2(kSinCosTab[2 * (i >> 3)], kSinCosTab[2 * (i >> 3) + 1]);
   for (int i = threadIdx.x; i < 32; i += blockDim.x) S.tab_exp[i] = kExp2Tab[i];
 }
 
