@@ -367,23 +367,36 @@ def main():
     rng = np.random.default_rng(rank)
     acts_np = acts_h.numpy().reshape(-1)
     # host policy: a uniform legal action per agent from its returned 5-bit mask
-    # (lookup of the j-th set bit, j = floor(u * #legal))
+    # (lookup of the j-th set bit, j = floor(u * #legal)), vectorised with
+    # preallocated buffers and 1-D takes
     kth = np.zeros((32, 5), np.int32)
-    n_legal = np.zeros(32, np.float64)
+    n_legal = np.zeros(32, np.float32)
     for code in range(32):
         bits = [b for b in range(5) if (code >> b) & 1]
         n_legal[code] = len(bits)
         kth[code, :len(bits)] = bits
-    u = np.empty(n_loc * A)
+    kth_flat = kth.reshape(-1)
+    n_ag = n_loc * A
+    u = np.empty(n_ag, np.float32)
+    code = np.empty(n_ag, np.uint8)
+    tmp = np.empty(n_ag, np.uint8)
+    flat = np.empty(n_ag, np.int64)
+
+    def host_policy(mv):
+        np.bitwise_or(mv[:, 0], np.left_shift(mv[:, 1], 1, out=tmp), out=code)
+        for b in (2, 3, 4):
+            np.bitwise_or(code, np.left_shift(mv[:, b], b, out=tmp), out=code)
+        rng.random(out=u, dtype=np.float32)
+        np.multiply(u, n_legal.take(code), out=u)
+        flat[:] = u                      # floor (u * #legal) < #legal
+        np.add(flat, code.astype(np.int64) * 5, out=flat)
+        kth_flat.take(flat, out=acts_np)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        mv = host["masks"].numpy().reshape(-1, 5)
-        code = mv[:, 0] | (mv[:, 1] << 1) | (mv[:, 2] << 2) | (mv[:, 3] << 3) | (mv[:, 4] << 4)
-        rng.random(out=u)
-        acts_np[:] = kth[code, (u * n_legal[code]).astype(np.int64)]
+        host_policy(host["masks"].numpy().reshape(-1, 5))
         venv.step(acts_h)
         venv.copy_outputs_into({"masks": host["masks"]})
         venv.copy_outputs_async(rest, copy_stream.cuda_stream)
