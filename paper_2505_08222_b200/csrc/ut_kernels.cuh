@@ -1106,17 +1106,21 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     // merged result equals the sequential one to rounding; otherwise (or with a
     // non-finite shift) the exact sequential path runs. The argument holds for
     // any UPPER BOUND s'_j >= s_j (e only shrinks, the guard stays
-    // conservative), so the stage maxima are taken in fp32 rounded up.
+    // conservative), so the stage maxima are taken from the high words only.
     double L[PPT];
 #pragma unroll
     for (int q = 0; q < PPT; ++q) L[q] = 0.0;
     float* mb = reinterpret_cast<float*>(R.buf());  // per-stage warp maxima, [stage * 32 + warp]
     // one stage: every particle's log-likelihood for measurement j, added to L in
     // stage order, and the stage's warp maximum (rounded up to fp32)
-    auto stage = [&](int j) -> float {
+    // Every ll is <= 0, so its high word, read as unsigned, grows with |ll|: the
+    // smallest high word is that of the largest ll, and as a double with a zero
+    // low word it is an upper bound of it (the mantissa is truncated toward 0).
+    // One unsigned min per particle and one REDUX per stage give s'_j.
+    auto stage = [&](int j) -> uint32_t {
       const double* m = S.meas + kMeasStride * ml[j];
       const double ox = m[0], oy = m[1], r2 = m[2], c2 = m[4];
-      float mj = -CUDART_INF_F;
+      uint32_t mj = 0xFFFFFFFFu;
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         if (FULL || k0 + q < P) {
@@ -1125,26 +1129,21 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           const double tq = d - r2;
           const double ll = (tq * tq) * c2;  // -(1/2)((d - r)/sigma)^2 to a few ulp
           L[q] = L[q] + ll;
-          mj = fmaxf(mj, __double2float_ru(ll));
+          mj = min(mj, (uint32_t)__double2hiint(ll));
         }
       }
       return mj;
     };
-    // warp max of a stage through an order-preserving int key (one REDUX
-    // instead of 5 shuffles)
-    auto stage_max = [&](int j, float mj) {
-      int key = __float_as_int(mj);
-      key ^= (key >> 31) & 0x7fffffff;
-      key = __reduce_max_sync(0xffffffffu, key);
-      key ^= (key >> 31) & 0x7fffffff;
-      if (lane == 0) mb[j * 32 + warp] = __int_as_float(key);
+    auto stage_max = [&](int j, uint32_t mj) {
+      mj = __reduce_min_sync(0xffffffffu, mj);
+      if (lane == 0) reinterpret_cast<uint32_t*>(mb)[j * 32 + warp] = mj;
     };
     // two stages per iteration so their distance / sqrt chains interleave (the
     // warp reductions, whose divergence check fences the scheduler, follow both)
 #pragma unroll 1
     for (int j = 0; j + 1 < nm; j += 2) {
-      const float m0 = stage(j);
-      const float m1 = stage(j + 1);
+      const uint32_t m0 = stage(j);
+      const uint32_t m1 = stage(j + 1);
       stage_max(j, m0);
       stage_max(j + 1, m1);
     }
@@ -1153,18 +1152,20 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     __syncthreads();
     double shift = 0.0;  // sum_j s'_j, in stage order
 #pragma unroll 1
+    const uint32_t* mbu = reinterpret_cast<const uint32_t*>(mb);
     for (int j = 0; j < nm; ++j) {
-      float sj = mb[j * 32];
+      uint32_t hj = mbu[j * 32];
       if constexpr (NW > 0 && NW % 4 == 0) {
 #pragma unroll
         for (int v = 0; v < NW; v += 4) {
-          const float4 m4 = *reinterpret_cast<const float4*>(mb + j * 32 + v);
-          sj = fmaxf(fmaxf(sj, m4.x), fmaxf(m4.y, fmaxf(m4.z, m4.w)));
+          const uint4 m4 = *reinterpret_cast<const uint4*>(mbu + j * 32 + v);
+          hj = min(hj, min(min(m4.x, m4.y), min(m4.z, m4.w)));
         }
       } else {
-        for (int v = 1; v < nw; ++v) sj = fmaxf(sj, mb[j * 32 + v]);
+        for (int v = 1; v < nw; ++v) hj = min(hj, mbu[j * 32 + v]);
       }
-      shift = j == 0 ? (double)sj : shift + (double)sj;
+      const double sj = __hiloint2double((int)hj, 0);  // >= max_i ll_ij
+      shift = j == 0 ? sj : shift + sj;
     }
     if (!isfinite(shift)) {
       exact = true;
