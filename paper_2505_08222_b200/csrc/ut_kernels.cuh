@@ -807,13 +807,13 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
   // ~1e-13 of an integer; the block-tree cumulative weights already differ
   // from the reference's sequential ones by ~1e-15 (x n = 1e-12), so exact
   // boundary tests would not make a flip any less likely.
-  auto count_le = [&](double cv) -> int {
-    const double x = cv * (double)P - u0;
-    return x < 0.0 ? 0 : (x >= (double)P ? P : (int)x + 1);
-  };
+  // As (base + loc) n + (1 - u0) >= 0, truncation gives the +1 and the clamp at
+  // 0 for free: count = min(n, trunc(loc n + (base n + 1 - u0))).
+  const double c0 = fma(base, (double)P, 1.0 - u0);
   int hq[PPT];  // count(cum[k]); P = no mark (the last particle, padding)
 #pragma unroll
-  for (int q = 0; q < PPT; ++q) hq[q] = k0 + q < P - 1 ? count_le(base + loc[q]) : P;
+  for (int q = 0; q < PPT; ++q)
+    hq[q] = k0 + q < P - 1 ? min(P, __double2int_rz(fma(loc[q], (double)P, c0))) : P;
   // Of a run of consecutive particles with the same count only the last one's
   // mark survives the max, so only it issues the atomic (lane 31's last always
   // does): the same marks with ~P spread atomics instead of P + conflicts.
