@@ -870,6 +870,22 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
   // the set buffer is next written by the prefetch after this set's estimate barrier
 }
 
+// One field of this thread's PPT consecutive particles to / from the set
+// buffer (128-bit accesses; k0 is a multiple of PPT).
+template <int PPT>
+__device__ __forceinline__ void store_field(double* f, int k0, const double (&v)[PPT]) {
+#pragma unroll
+  for (int q = 0; q < PPT; q += 2) *reinterpret_cast<double2*>(f + k0 + q) = make_double2(v[q], v[q + 1]);
+}
+template <int PPT>
+__device__ __forceinline__ void load_field(const double* f, int k0, double (&v)[PPT]) {
+#pragma unroll
+  for (int q = 0; q < PPT; q += 2) {
+    const double2 t = *reinterpret_cast<const double2*>(f + k0 + q);
+    v[q] = t.x, v[q + 1] = t.y;
+  }
+}
+
 // Per-phase cycle profile of the particle-set loop (debug builds with
 // -DUT_SET_PROFILE only; thread 0 of each CTA, read by ut_debug_set_profile).
 constexpr int kSetProfSlots = 12;
@@ -1044,6 +1060,13 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       }
     }
   }
+  const int nm = S.mcount[ti];
+  bool exact = nm > kMaxMerged || B.force_exact;
+  // merged pass: w, vx, vy leave the registers during the likelihood stages
+  // (the set buffer keeps them in this thread's own slots until the barrier
+  // after which the staging may start)
+  const bool merged = nm > 0 && !exact;
+  const int NPf = (int)(S.cum - S.pf) / 4;  // field stride of the set buffer
   if (FULL) {
     SETPROF(0);
     mbar_wait_sa(S.mbar_sa, tphase);
@@ -1055,11 +1078,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       const double2 y = *reinterpret_cast<const double2*>(S.pf + P + k0 + q);
       const double2 u = *reinterpret_cast<const double2*>(S.pf + 2 * P + k0 + q);
       const double2 v = *reinterpret_cast<const double2*>(S.pf + 3 * P + k0 + q);
-      const double2 w = *reinterpret_cast<const double2*>(S.pf + 4 * P + k0 + q);
       s.px[q] = x.x, s.px[q + 1] = x.y, s.py[q] = y.x, s.py[q + 1] = y.y;
       s.vx[q] = u.x, s.vx[q + 1] = u.y, s.vy[q] = v.x, s.vy[q + 1] = v.y;
-      s.w[q] = w.x, s.w[q + 1] = w.y;
     }
+    if (!merged) load_field<PPT>(S.pf + 4 * NPf, k0, s.w);
   }
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
@@ -1090,11 +1112,14 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 
   // ---- range updates: own ping, then fused senders (env.cpp:356-360, 385-392)
   SETPROF(2);
-  const int nm = S.mcount[ti];
   const uint16_t* ml = S.mlist + ti * c.sA;
   bool have_ess = false;
   double ess = 0.0;
-  bool exact = nm > kMaxMerged || B.force_exact;
+  if (merged) {
+    store_field<PPT>(S.pf + 2 * NPf, k0, s.vx);
+    store_field<PPT>(S.pf + 3 * NPf, k0, s.vy);
+    if (!FULL) store_field<PPT>(S.pf + 4 * NPf, k0, s.w);
+  }
   if (nm > 0 && !exact) {
     // Merged pass. With L_i = sum_j ll_ij and s_j = max_i ll_ij, the sequential
     // reference computes e_i / sum(e) with e_i = w_i exp(L_i - sum_j s_j), up to
@@ -1148,6 +1173,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       stage_max(j + 1, m1);
     }
     if (nm & 1) stage_max(nm - 1, stage(nm - 1));
+    if (merged) load_field<PPT>(S.pf + 4 * NPf, k0, s.w);
     SETPROF(3);
     __syncthreads();
     double shift = 0.0;  // sum_j s'_j, in stage order
@@ -1169,6 +1195,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     }
     if (!isfinite(shift)) {
       exact = true;
+      if (merged) {  // before the exact path's staging barrier
+        load_field<PPT>(S.pf + 2 * NPf, k0, s.vx);
+        load_field<PPT>(S.pf + 3 * NPf, k0, s.vy);
+      }
     } else {
       double e[PPT], ls = 0.0, lq = 0.0;
       int lx = 0;  // max biased exponent of e
@@ -1181,6 +1211,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           lq = lq + e[q] * e[q];
           lx = max(lx, __double2hiint(e[q]) >> 20);
         }
+      }
+      if (merged) {  // before the barrier after which the staging may start
+        load_field<PPT>(S.pf + 2 * NPf, k0, s.vx);
+        load_field<PPT>(S.pf + 3 * NPf, k0, s.vy);
       }
       SETPROF(4);
       const double2 r = R.sum2_imax<NW>(ls, lq, lx);
