@@ -822,7 +822,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     const int hn = q + 1 < PPT ? hq[q + 1] : nxt;
-    if (hq[q] < P && hq[q] != hn) atomicMax(&mark[hq[q]], k0 + q + 1);
+    red_max_shared_if(hq[q] < P && hq[q] != hn, mark + min(hq[q], P - 1), k0 + q + 1);
   }
   __syncthreads();
   int r[PPT];
@@ -1161,7 +1161,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     };
     auto stage_max = [&](int j, uint32_t mj) {
       mj = __reduce_min_sync(0xffffffffu, mj);
-      if (lane == 0) reinterpret_cast<uint32_t*>(mb)[j * 32 + warp] = mj;
+      st_shared_if(lane == 0, reinterpret_cast<uint32_t*>(mb) + j * 32 + warp, mj);
     };
     // two stages per iteration so their distance / sqrt chains interleave (the
     // warp reductions, whose divergence check fences the scheduler, follow both)
