@@ -780,7 +780,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
   }
   double excl = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) excl = 0.0;
-  if (lane == 31) wsum[warp] = incl;
+  st_shared_if(lane == 31, wsum + warp, incl);
   static_assert(PPT % 4 == 0, "mark zeroing takes whole int4s");
   if (FULL || k0 < P) {
 #pragma unroll
@@ -847,7 +847,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
   const int wtop = __shfl_sync(0xffffffffu, mi, top);
   if (!below) mex = -1;
   int* wmx = reinterpret_cast<int*>(wsum + 96);
-  if (lane == 31) wmx[warp] = wtop;
+  st_shared_if(lane == 31, reinterpret_cast<uint32_t*>(wmx) + warp, (uint32_t)wtop);
   __syncthreads();
   if constexpr (NW > 0) {
 #pragma unroll
@@ -982,7 +982,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll
       for (int i = 0; i < NB; ++i) blk[q][i] = bo[q * NB + i];
     const uint4 ex = bo[4 * NB];
-    if (lane < 4) S.xch[warp * 5 + lane] = ex;
+    st_shared_if(lane < 4, S.xch + warp * 5 + (lane & 3), ex);
     if (warp == nw - 1 && lane == 3) {
       const uint4 y = off == 3 ? philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P + 1) : ex;
       uint32_t w2[4];
@@ -1016,7 +1016,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         nb.x = __shfl_down_sync(0xffffffffu, blk[q][0].x, 1);
         nb.y = __shfl_down_sync(0xffffffffu, blk[q][0].y, 1);
         nb.z = __shfl_down_sync(0xffffffffu, blk[q][0].z, 1);
-        if (off != 0 && lane == 31) nb = S.xch[warp * 5 + q];
+        const uint4 xq = S.xch[warp * 5 + q];  // broadcast load, selected on lane 31
+        if (off != 0 && lane == 31) nb = xq;
         uint32_t a[4 * NB + 3];
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
