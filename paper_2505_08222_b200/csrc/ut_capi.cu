@@ -409,7 +409,11 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   UT_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   // FULL instances: P == nt * PPT with a compile-time particle capacity
-  v->full = (v->P == v->nt * kPPT) && (v->P == 1024 || v->P == 512 || v->P == 256);
+  // FULL instances also assume particle noise (every config of the batch has it):
+  // noise-free configs (test scenarios) take the generic instance
+  bool all_noise = true;
+  for (const DevConfig& d : v->dcfgs) all_noise = all_noise && d.noise_on != 0;
+  v->full = (v->P == v->nt * kPPT) && (v->P == 1024 || v->P == 512 || v->P == 256) && all_noise;
   v->np = v->full ? v->P : 1024;
   const void* fn = nullptr;
   if (v->np == 1024 && v->full) {

@@ -934,7 +934,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   const uint64_t pos = (uint64_t)tk[TK_POS];
   const uint64_t key = (uint64_t)__double_as_longlong(tk[TK_KEY]);
   const int off = (int)(pos & 3);
-  const bool noise = c.noise_on != 0;
+  const bool noise = FULL || c.noise_on != 0;  // FULL instances run only with noise (host side)
   const uint64_t u0p = pos + (noise ? 4ull * (uint64_t)P : 0ull);  // resample draw follows predict
 
   // ---- particles into registers (FULL: after the noise is drawn, below, so the
