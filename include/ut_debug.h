@@ -22,7 +22,9 @@ int ut_debug_philox(uint64_t key, uint64_t stream, uint64_t block0, int32_t n, i
 struct ut_vecenv;
 /* Verification knobs: force_exact != 0 makes every particle set take the exact
  * sequential update path (tracking.cpp:119-143 once per measurement) instead of
- * the merged one; trace_env >= 0 printf's a per-set trace for that env. */
+ * the merged one; trace_env >= 0 printf's a per-set trace for that env (only
+ * in the generic step instance: particle counts other than 256/512/1024 or
+ * noise-free configs). */
 int ut_debug_set_knobs(struct ut_vecenv* v, int force_exact, int64_t trace_env);
 /* Per-CTA cycle totals of the step kernel since phase timing was enabled
  * (ut_vecenv_enable_phase_timing): *n = grid size; out may be NULL to query it.

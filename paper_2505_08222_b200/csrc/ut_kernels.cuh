@@ -1098,17 +1098,16 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     }
   }
   const double ms = tk[TK_MAXSPEED];
-  if (ms > 0.0) {
+  // branch-free (no clamp when ms <= 0, tracking.cpp:105): the quotient is
+  // formed for every particle (sp = 0 or ms <= 0 give values the select drops)
+  const bool clamp_on = ms > 0.0;
 #pragma unroll
-    for (int j = 0; j < PPT; ++j) {
-      const double sp = sqrt_rn_clamp(s.vx[j] * s.vx[j] + s.vy[j] * s.vy[j]);
-      // branch-free: the quotient is formed for every particle (sp = 0 gives
-      // inf/NaN, discarded by the select)
-      const double qt = div_rn_clamp(ms, sp);
-      const double f = sp > ms ? qt : 1.0;
-      s.vx[j] = s.vx[j] * f;
-      s.vy[j] = s.vy[j] * f;
-    }
+  for (int j = 0; j < PPT; ++j) {
+    const double sp = sqrt_rn_clamp(s.vx[j] * s.vx[j] + s.vy[j] * s.vy[j]);
+    const double qt = div_rn_clamp(ms, sp);
+    const double f = clamp_on && sp > ms ? qt : 1.0;
+    s.vx[j] = s.vx[j] * f;
+    s.vy[j] = s.vy[j] * f;
   }
 
   // ---- range updates: own ping, then fused senders (env.cpp:356-360, 385-392)
@@ -1279,7 +1278,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     }
   }
 
-  if (B.trace_env == (int64_t)e && tid == 0)
+  if (!FULL && B.trace_env == (int64_t)e && tid == 0)  // trace: generic instance only
     printf("[trace env %lld set %d] nm=%d exact=%d have_ess=%d ess=%.17g resampled=%d pos=%llu\n",
            (long long)e, ps, nm, (int)exact, (int)have_ess, ess, (int)resampled,
            (unsigned long long)pos);  // at set start
