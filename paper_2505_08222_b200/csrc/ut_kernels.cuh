@@ -1177,7 +1177,6 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     SETPROF(3);
     __syncthreads();
     double shift = 0.0;  // sum_j s'_j, in stage order
-#pragma unroll 1
     const uint32_t* mbu = reinterpret_cast<const uint32_t*>(mb);
     for (int j = 0; j < nm; ++j) {
       uint32_t hj = mbu[j * 32];
