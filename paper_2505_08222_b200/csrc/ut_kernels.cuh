@@ -1160,7 +1160,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       return mj;
     };
     auto stage_max = [&](int j, uint32_t mj) {
-      mj = __reduce_min_sync(0xffffffffu, mj);
+      mj = redux_min_u32(mj);
       st_shared_if(lane == 0, reinterpret_cast<uint32_t*>(mb) + j * 32 + warp, mj);
     };
     // two stages per iteration so their distance / sqrt chains interleave (the
