@@ -1282,16 +1282,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
            (long long)e, ps, nm, (int)exact, (int)have_ess, ess, (int)resampled,
            (unsigned long long)pos);  // at set start
 
-  // ---- estimate (env.cpp:403-407)
-  // The set buffer is free once every thread is past the estimate barrier: the
-  // next set of this chunk is prefetched into it then (generic-proxy writes to
-  // it are fenced against the async-proxy copy first).
-  if (FULL) fence_proxy_async();
-  SETPROF(8);
-  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R, resampled, c.inv_P);
-  SETPROF(9);
-  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
-  // ---- the set back to HBM
+  // ---- the set back to HBM (ahead of the estimate, which only reads the
+  // registers: the store queue drains under the estimate's reduction)
   const size_t base = (size_t)gset * P;
   if (FULL) {
     // 256-bit stores (STG.E.ENL2.256): one per field and 4 particles
@@ -1316,6 +1308,15 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       }
     }
   }
+  // ---- estimate (env.cpp:403-407)
+  // The set buffer is free once every thread is past the estimate barrier: the
+  // next set of this chunk is prefetched into it then (generic-proxy writes to
+  // it are fenced against the async-proxy copy first).
+  if (FULL) fence_proxy_async();
+  SETPROF(8);
+  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R, resampled, c.inv_P);
+  SETPROF(9);
+  if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
   if (tid == 0) {
     const Rec rec = rec_of(B, e);
     TRK(K_EX, ti) = est.x;
