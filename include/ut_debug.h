@@ -26,7 +26,8 @@ struct ut_vecenv;
  * in the generic step instance: particle counts other than 256/512/1024 or
  * noise-free configs). */
 int ut_debug_set_knobs(struct ut_vecenv* v, int force_exact, int64_t trace_env);
-/* Per-CTA cycle totals of the step kernel since phase timing was enabled
+/* Per-CTA busy cycles (every phase, not the grid-barrier waits) of the step
+ * kernel since phase timing was enabled
  * (ut_vecenv_enable_phase_timing): *n = grid size; out may be NULL to query it.
  * Shows the load balance of the persistent grid. */
 int ut_debug_cta_cycles(struct ut_vecenv* v, uint64_t* out, int64_t cap, int64_t* n);
@@ -41,6 +42,10 @@ int ut_debug_fp64_peak(int device, double* dfma_per_s);
  * weight sums, exact/ESS, resample, store, estimate, tail). Non-zero only in
  * builds with -DUT_SET_PROFILE (A/B diagnostics). */
 int ut_debug_set_profile(int device, uint64_t* out, int reset);
+/* Which step-kernel instance the handle launches: *full = 1 for the TMA /
+ * register-tile instance (P in {256, 512, 1024}, particle noise on), 0 for the
+ * generic one; *np = its compile-time particle capacity. */
+int ut_debug_instance(struct ut_vecenv* v, int32_t* full, int32_t* np);
 /* derive_key (rng.hpp:30-38) evaluated on the device. */
 int ut_debug_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t d, int device, uint64_t* out);
 #ifdef __cplusplus

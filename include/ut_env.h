@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define UT_ABI_VERSION 2
+#define UT_ABI_VERSION 3
 
 enum ut_status {
   UT_OK = 0,
@@ -91,9 +91,13 @@ typedef struct ut_buffers {
   uint8_t* collision;      /* StepOutput::collision (env.hpp:56) */
   int32_t* step;           /* WorldState::step per env (env.hpp:50) */
   int32_t* actions;        /* device action staging, n_envs * n_agents */
-  /* particle store, structure-of-arrays: field[set * n_particles + k],
-   * set = env * n_agents * n_targets + agent * n_targets + target */
+  /* particle store, structure-of-arrays: field[set * n_particles + k] for
+   * set = set_offset[env] + agent * n_targets(env) + target; a homogeneous
+   * batch has set_offset == NULL and set = env * n_agents * n_targets + ...
+   * (mixed fleets, ut_vecenv_create_mixed, store only their own A_e * T_e sets) */
   double *px, *py, *vx, *vy, *w;
+  int64_t total_sets;          /* sets in the store (sum over envs of A_e * T_e) */
+  const int64_t* set_offset;   /* device, [n_envs], or NULL when homogeneous */
 } ut_buffers;
 
 /* Host destinations for ut_vecenv_copy_outputs(); NULL members are skipped. */
@@ -136,6 +140,20 @@ enum {
   UT_N_STATS
 };
 
+/* Phases of the step (StepPhase, env.hpp:71-80; PhaseTimer env.cpp:18-36,
+ * 250-279) plus the auto-reset, which the reference runs outside its phase
+ * timers (vecenv.cpp:140). On the device each CTA times its own share of the
+ * grid (SM clock of thread 0, converted to ns), summed over CTAs like the
+ * reference sums its envs' timers (vecenv.cpp:160-173). The merged range-update
+ * pass of a particle set is split between FILTER (the agent's own ping,
+ * env.cpp:356-360) and COMMS (the fused senders' pings, env.cpp:385-392) in
+ * proportion; COMMS also holds the comm decisions, maybe_resample and the
+ * estimate (env.cpp:365-410). */
+enum {
+  UT_PHASE_TARGETS = 0, UT_PHASE_AGENTS, UT_PHASE_MEASURE, UT_PHASE_FILTER, UT_PHASE_COMMS,
+  UT_PHASE_OBSERVE, UT_PHASE_REWARD, UT_PHASE_RESET, UT_N_PHASES
+};
+
 /* BenchmarkReport (vecenv.hpp:87-98), device-timed. */
 typedef struct ut_benchmark_report {
   int64_t n_envs;
@@ -143,6 +161,8 @@ typedef struct ut_benchmark_report {
   double wall_seconds; /* CUDA-event time of the timed steps */
   double sps;          /* env-steps per second, n_envs * steps / seconds (vecenv.cpp:198) */
   double agent_sps;    /* sps * n_agents */
+  uint64_t phase_ns[UT_N_PHASES]; /* BenchmarkReport::phase_ns (+ reset), CTA-summed */
+  uint64_t total_ns;              /* BenchmarkReport::total_ns: sum of the seven step phases */
 } ut_benchmark_report;
 
 typedef struct ut_vecenv ut_vecenv;
@@ -194,8 +214,17 @@ int ut_vecenv_set_output_buffers(ut_vecenv* v, int n);
 /* Enqueues the D2H copies of the current outputs on `cuda_stream` after the
  * handle's pending work, and returns; synchronize that stream before reading. */
 int ut_vecenv_copy_outputs_async(ut_vecenv* v, const ut_host_outputs* dst, void* cuda_stream);
-/* Runs subsequent work on a caller-owned cudaStream_t (NULL = the handle's own). */
+/* Runs subsequent work on a caller-owned cudaStream_t. NULL selects the
+ * handle's own (non-blocking) stream; UT_STREAM_LEGACY (the value of
+ * cudaStreamLegacy) selects the legacy default stream, which is what a
+ * framework's stream handle 0 means (e.g. torch.cuda.current_stream()). */
+#define UT_STREAM_LEGACY ((void*)0x1)
 int ut_vecenv_set_stream(ut_vecenv* v, void* cuda_stream);
+/* Orders the handle's next work after everything enqueued so far on
+ * `cuda_stream` (0 = the legacy default stream, as in CUDA): call it before
+ * ut_vecenv_step with actions a device policy is still producing, or before a
+ * step that will overwrite outputs other kernels are still reading. */
+int ut_vecenv_wait_stream(ut_vecenv* v, void* cuda_stream);
 int ut_vecenv_synchronize(ut_vecenv* v);
 /* Reads (and optionally zeroes) the device statistics vector. */
 int ut_vecenv_stats(ut_vecenv* v, double out[UT_N_STATS], int reset);
@@ -203,13 +232,17 @@ int ut_vecenv_stats(ut_vecenv* v, double out[UT_N_STATS], int reset);
 int64_t ut_vecenv_launch_count(const ut_vecenv* v);
 
 /* VecEnv::enable_phase_timing / reset_timing / phase_ns (vecenv.hpp:64-67,
- * PhaseTimer env.cpp:18-36) on the device: per-env SM clock cycles spent in
- * UT_PHASE_* summed over envs. The seven reference phases map onto four:
- * targets+agents+measure+comm decisions -> PROLOGUE; filter + fused comm
- * updates -> FILTER; observe + reward -> OUTPUT; auto-reset -> RESET. */
-enum { UT_PHASE_PROLOGUE = 0, UT_PHASE_FILTER, UT_PHASE_OUTPUT, UT_PHASE_RESET, UT_N_PHASES };
+ * PhaseTimer env.cpp:18-36) on the device, per UT_PHASE_* (see above): SM
+ * cycles, or ns at the SM clock rate the timed launches ran at. */
 int ut_vecenv_enable_phase_timing(ut_vecenv* v, int on);
 int ut_vecenv_phase_cycles(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset);
+int ut_vecenv_phase_ns(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset);
+
+/* Auto-reset of finished envs inside step / step_policy (vecenv.cpp:106-112,
+ * 140; default on). Off gives the single Environment's semantics
+ * (env.cpp:234-504): a finished env keeps its terminal state and stays done
+ * until reset; final_obs is not written. */
+int ut_vecenv_set_auto_reset(ut_vecenv* v, int on);
 
 /* ---- per-env state (Environment API) ----------------------------------- */
 /* Environment::serialize_state / deserialize_state (env.cpp:550-659), identical

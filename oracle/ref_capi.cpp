@@ -190,6 +190,58 @@ int ref_env_world_step(void* h, int64_t env, int32_t* step) {
   return guarded([&] { *step = static_cast<RefVec*>(h)->venv->env(static_cast<int>(env)).world().step; });
 }
 
+// A single reference Environment (env.hpp:91-171): no auto-reset, done stays set.
+struct RefEnv {
+  EnvConfig cfg;
+  std::unique_ptr<Environment> env;
+};
+
+int ref_env_create(const ut_env_config* c, uint64_t seed, int64_t env_index, void** out) {
+  return guarded([&] {
+    auto r = std::make_unique<RefEnv>();
+    r->cfg = to_ref(*c);
+    r->env = std::make_unique<Environment>(r->cfg, seed, static_cast<int>(env_index));
+    *out = r.release();
+  });
+}
+
+void ref_env_destroy(void* h) { delete static_cast<RefEnv*>(h); }
+
+int ref_env_reset(void* h) {
+  return guarded([&] { static_cast<RefEnv*>(h)->env->reset(); });
+}
+
+// Environment::step; reward / done / collision of the StepOutput (env.hpp:53-60).
+int ref_env_step(void* h, const int32_t* actions, double* reward, int32_t* done, int32_t* collision) {
+  return guarded([&] {
+    Environment& e = *static_cast<RefEnv*>(h)->env;
+    const StepOutput& o =
+        e.step(std::span<const int>(reinterpret_cast<const int*>(actions), static_cast<std::size_t>(e.config().n_agents)));
+    *reward = o.reward;
+    *done = o.done ? 1 : 0;
+    *collision = o.collision ? 1 : 0;
+  });
+}
+
+int ref_env_serialize_one(void* h, double* blob, size_t cap, size_t* len) {
+  return guarded([&] {
+    const std::vector<double> b = static_cast<RefEnv*>(h)->env->serialize_state();
+    *len = b.size();
+    if (blob == nullptr) return;
+    if (cap < b.size()) throw DataError("serialize: buffer too small");
+    std::memcpy(blob, b.data(), sizeof(double) * b.size());
+  });
+}
+
+// Environment::observation(a) (env.hpp:109-110): R x 12, row-major here.
+int ref_env_observation(void* h, int32_t agent, double* out) {
+  return guarded([&] {
+    const Eigen::MatrixXd& m = static_cast<RefEnv*>(h)->env->observation(agent);
+    for (int r = 0; r < m.rows(); ++r)
+      for (int k = 0; k < m.cols(); ++k) out[r * m.cols() + k] = m(r, k);
+  });
+}
+
 // benchmark_sps (vecenv.cpp:175-202): SPS plus the seven phase sums.
 int ref_benchmark_sps(const ut_env_config* c, int64_t n_envs, int32_t n_steps, int policy, uint64_t seed,
                       int32_t workers, int32_t warmup, double* sps, double* wall_seconds,

@@ -12,6 +12,10 @@ UT_FEATURE_DIM = 12
 UT_REWARD_TRACKING, UT_REWARD_FOLLOW = 0, 1
 UT_POLICY_RANDOM, UT_POLICY_SCRIPTED = 0, 1
 UT_HEADING_DEFAULT, UT_HEADING_BUCKET = 0, 1
+UT_STREAM_LEGACY = 1  # cudaStreamLegacy
+# UT_PHASE_* (ut_env.h): the reference's seven StepPhase values, then the auto-reset
+PHASE_NAMES = ("targets", "agents", "measure", "filter", "comms", "observe", "reward", "reset")
+UT_N_PHASES = len(PHASE_NAMES)
 
 STAT_NAMES = (
     "env_steps", "reward_sum", "track_err_sum", "episodes_done", "episode_return_sum",
@@ -19,7 +23,7 @@ STAT_NAMES = (
     "eval_dist_sum", "eval_dist_sq", "eval_err_sum", "eval_err_sq", "eval_collided_episodes",
     "eval_lost_episodes",
 )
-UT_ABI_VERSION = 2
+UT_ABI_VERSION = 3
 UT_N_STATS = len(STAT_NAMES)
 
 
@@ -67,6 +71,7 @@ class Buffers(C.Structure):
         ("actions", C.c_void_p),
         ("px", C.c_void_p), ("py", C.c_void_p), ("vx", C.c_void_p), ("vy", C.c_void_p),
         ("w", C.c_void_p),
+        ("total_sets", C.c_int64), ("set_offset", C.c_void_p),
     ]
 
 
@@ -84,6 +89,7 @@ class BenchmarkReport(C.Structure):
         ("n_envs", C.c_int64), ("n_agents", C.c_int32), ("n_targets", C.c_int32),
         ("timed_steps", C.c_int32), ("_pad0", C.c_int32),
         ("wall_seconds", C.c_double), ("sps", C.c_double), ("agent_sps", C.c_double),
+        ("phase_ns", C.c_uint64 * UT_N_PHASES), ("total_ns", C.c_uint64),
     ]
 
 
@@ -108,6 +114,9 @@ def declare_product(lib):
         "ut_vecenv_buffers": (C.c_int, [P, C.POINTER(Buffers)]),
         "ut_vecenv_copy_outputs": (C.c_int, [P, C.POINTER(HostOutputs)]),
         "ut_vecenv_set_stream": (C.c_int, [P, P]),
+        "ut_vecenv_wait_stream": (C.c_int, [P, P]),
+        "ut_vecenv_set_auto_reset": (C.c_int, [P, C.c_int]),
+        "ut_vecenv_phase_ns": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int]),
         "ut_vecenv_set_output_buffers": (C.c_int, [P, C.c_int]),
         "ut_vecenv_capture_trajectory": (C.c_int, [P, I64, I64]),
         "ut_vecenv_trajectory_rows": (C.c_int, [P, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_size_t)]),
@@ -154,6 +163,8 @@ def declare_debug(lib):
     lib.ut_debug_ieee_check.restype = C.c_int
     lib.ut_debug_set_knobs.argtypes = [C.c_void_p, C.c_int, C.c_int64]
     lib.ut_debug_set_knobs.restype = C.c_int
+    lib.ut_debug_instance.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    lib.ut_debug_instance.restype = C.c_int
     return lib
 
 
@@ -165,6 +176,7 @@ PRODUCT_SYMBOLS = (
     "ut_env_serialize", "ut_env_deserialize", "ut_env_world_step", "ut_benchmark_sps",
     "ut_vecenv_export_state", "ut_vecenv_import_state", "ut_vecenv_set_output_buffers",
     "ut_vecenv_copy_outputs_async", "ut_vecenv_capture_trajectory", "ut_vecenv_trajectory_rows",
-    "ut_vecenv_enable_phase_timing", "ut_vecenv_phase_cycles",
+    "ut_vecenv_enable_phase_timing", "ut_vecenv_phase_cycles", "ut_vecenv_phase_ns",
+    "ut_vecenv_wait_stream", "ut_vecenv_set_auto_reset",
     "ut_last_error", "ut_abi_version",
 )

@@ -33,6 +33,20 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
+// Scoped current device: every entry point runs on the handle's device and
+// leaves the calling thread's current device as it found it.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 #define UT_CUDA(call)                                                                     \
   do {                                                                                    \
     cudaError_t err_ = (call);                                                            \
@@ -147,7 +161,7 @@ struct ut_vecenv {
 
   ~ut_vecenv() {
     if (stream) cudaStreamSynchronize(stream);
-    for (cudaEvent_t ev : {copy_done[0], copy_done[1], step_done})
+    for (cudaEvent_t ev : {copy_done[0], copy_done[1], step_done, order_ev})
       if (ev) cudaEventDestroy(ev);
     for (void* p : allocs) cudaFree(p);
     if (h_status) cudaFreeHost(h_status);
@@ -218,9 +232,12 @@ struct ut_vecenv {
 
   // Output double buffering (ut_vecenv_set_output_buffers): every step writes the
   // set the previous step did not, after any asynchronous copy still reading it
-  // (ut_vecenv_copy_outputs_async) has finished. final_obs is shared.
+  // (ut_vecenv_copy_outputs_async) has finished. final_obs is double-buffered
+  // too: a step only writes the rows of finished envs, so the set it writes is
+  // first brought up to date from the previous one.
   struct OutSet {
-    double *obs = nullptr, *global = nullptr, *rewards = nullptr, *track_err = nullptr, *min_dist = nullptr;
+    double *obs = nullptr, *final_obs = nullptr, *global = nullptr, *rewards = nullptr, *track_err = nullptr,
+           *min_dist = nullptr;
     uint8_t *dones = nullptr, *masks = nullptr, *lost = nullptr, *collision = nullptr;
     int32_t* step = nullptr;
   };
@@ -228,10 +245,11 @@ struct ut_vecenv {
   int n_out = 1, cur = 0;
   cudaEvent_t copy_done[2] = {nullptr, nullptr};
   cudaEvent_t step_done = nullptr;
+  cudaEvent_t order_ev = nullptr;  // ut_vecenv_wait_stream
 
   void bind_outputs(int k) {
     const OutSet& o = out[k];
-    B.obs = o.obs, B.global = o.global, B.rewards = o.rewards, B.track_err = o.track_err;
+    B.obs = o.obs, B.final_obs = o.final_obs, B.global = o.global, B.rewards = o.rewards, B.track_err = o.track_err;
     B.min_dist = o.min_dist, B.dones = o.dones, B.masks = o.masks, B.lost = o.lost;
     B.collision = o.collision, B.step = o.step;
   }
@@ -247,6 +265,8 @@ struct ut_vecenv {
     if (n_out == 2) {
       const int t = cur ^ 1;
       if ((rc = wait_outputs(t))) return rc;
+      UT_CUDA(cudaMemcpyAsync(out[t].final_obs, out[cur].final_obs, sizeof(double) * 12 * B.obs_rows,
+                              cudaMemcpyDeviceToDevice, stream));
       bind_outputs(t);
       cur = t;
       if ((rc = sync_batch())) return rc;
@@ -331,7 +351,7 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
     return fail(UT_ERR_CONFIG, "n_envs x agents x targets = %lld particle sets per device (max 2^31 - 2)",
                 (long long)v->total_sets);
 
-  UT_CUDA(cudaSetDevice(device));
+  DeviceGuard dg(device);
   UT_CUDA(cudaStreamCreateWithFlags(&v->own_stream, cudaStreamNonBlocking));
   v->stream = v->own_stream;
   UT_CUDA(cudaMallocHost(&v->h_status, 2 * sizeof(int32_t)));
@@ -383,7 +403,8 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   if ((rc = v->alloc(&B.lost, (size_t)(n_envs * Tm)))) return rc;
   if ((rc = v->alloc(&B.collision, (size_t)n_envs))) return rc;
   if ((rc = v->alloc(&B.step, (size_t)n_envs))) return rc;
-  v->out[0] = {B.obs, B.global, B.rewards, B.track_err, B.min_dist, B.dones, B.masks, B.lost, B.collision, B.step};
+  v->out[0] = {B.obs, B.final_obs, B.global, B.rewards, B.track_err, B.min_dist,
+               B.dones, B.masks, B.lost, B.collision, B.step};
   int32_t* acts;
   if ((rc = v->alloc(&acts, (size_t)(n_envs * Am)))) return rc;
   B.actions = acts;
@@ -395,6 +416,7 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   B.traj = nullptr;
   B.traj_lo = B.traj_hi = 0;
   B.phase_cycles = nullptr;
+  B.auto_reset = 1;
   // VecEnv ctor zero-fills every batch buffer (vecenv.cpp:26-38)
   UT_CUDA(cudaMemsetAsync(B.final_obs, 0, sizeof(double) * 12 * B.obs_rows, v->stream));
   UT_CUDA(cudaMemsetAsync(B.track_err, 0, sizeof(double) * n_envs * Tm, v->stream));
@@ -554,15 +576,21 @@ int ut_vecenv_create_mixed(const ut_env_config* cfgs, int32_t n_cfgs, const int3
   return finish_create(v, build(v, cfgs, n_cfgs, cfg_of_env, n_envs, master_seed, env_index_offset, device), out);
 }
 
-void ut_vecenv_destroy(ut_vecenv* v) { delete v; }
+void ut_vecenv_destroy(ut_vecenv* v) {
+  if (!v) return;
+  DeviceGuard dg(v->device);
+  delete v;
+}
 
 int ut_vecenv_reset_all(ut_vecenv* v) {
+  DeviceGuard dg(v->device);
   int rc;
   if ((rc = v->reset_status()) || (rc = v->launch_reset(0))) return rc;
   return v->check_status("reset_all");
 }
 
 int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device) {
+  DeviceGuard dg(v->device);
   const size_t n = (size_t)(v->n_envs * v->A_max);
   UT_CUDA(cudaMemcpyAsync(const_cast<int32_t*>(v->B.actions), actions, n * sizeof(int32_t),
                           actions_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, v->stream));
@@ -595,6 +623,7 @@ int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device) 
 }
 
 int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps) {
+  DeviceGuard dg(v->device);
   if (policy != UT_POLICY_RANDOM && policy != UT_POLICY_SCRIPTED)
     return fail(UT_ERR_CONTRACT, "step_policy: unknown policy %d", policy);
   int rc;
@@ -605,6 +634,7 @@ int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps) {
 }
 
 int ut_vecenv_refresh_outputs(ut_vecenv* v) {
+  DeviceGuard dg(v->device);
   int sms = 0, rc;
   UT_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, v->device));
   if ((rc = v->wait_outputs(v->cur))) return rc;
@@ -616,6 +646,7 @@ int ut_vecenv_refresh_outputs(ut_vecenv* v) {
 }
 
 int ut_vecenv_set_output_buffers(ut_vecenv* v, int n) {
+  DeviceGuard dg(v->device);
   if (n != 1 && n != 2) return fail(UT_ERR_CONTRACT, "set_output_buffers: n must be 1 or 2");
   if (n == v->n_out) return UT_OK;
   UT_CUDA(cudaStreamSynchronize(v->stream));
@@ -625,18 +656,21 @@ int ut_vecenv_set_output_buffers(ut_vecenv* v, int n) {
     const int64_t E = v->n_envs, Am = v->A_max, Tm = v->T_max;
     ut_vecenv::OutSet& o = v->out[1];
     int rc;
-    if ((rc = v->alloc(&o.obs, (size_t)(12 * v->B.obs_rows))) || (rc = v->alloc(&o.global, (size_t)(12 * v->B.global_rows))) ||
+    if ((rc = v->alloc(&o.obs, (size_t)(12 * v->B.obs_rows))) || (rc = v->alloc(&o.final_obs, (size_t)(12 * v->B.obs_rows))) ||
+        (rc = v->alloc(&o.global, (size_t)(12 * v->B.global_rows))) ||
         (rc = v->alloc(&o.rewards, (size_t)E)) || (rc = v->alloc(&o.dones, (size_t)E)) ||
         (rc = v->alloc(&o.masks, (size_t)(E * Am * 5))) || (rc = v->alloc(&o.track_err, (size_t)(E * Tm))) ||
         (rc = v->alloc(&o.min_dist, (size_t)(E * Tm))) || (rc = v->alloc(&o.lost, (size_t)(E * Tm))) ||
         (rc = v->alloc(&o.collision, (size_t)E)) || (rc = v->alloc(&o.step, (size_t)E)))
       return rc;
+    UT_CUDA(cudaMemsetAsync(o.final_obs, 0, sizeof(double) * 12 * v->B.obs_rows, v->stream));
   }
   if (n == 1 && v->cur == 1) {  // keep the current outputs in set 0
     const ut_vecenv::OutSet &a = v->out[0], &b = v->out[1];
     const int64_t E = v->n_envs, Am = v->A_max, Tm = v->T_max;
     auto cp = [&](void* d, const void* s2, size_t bytes) { return cudaMemcpyAsync(d, s2, bytes, cudaMemcpyDeviceToDevice, v->stream); };
     UT_CUDA(cp(a.obs, b.obs, sizeof(double) * 12 * v->B.obs_rows));
+    UT_CUDA(cp(a.final_obs, b.final_obs, sizeof(double) * 12 * v->B.obs_rows));
     UT_CUDA(cp(a.global, b.global, sizeof(double) * 12 * v->B.global_rows));
     UT_CUDA(cp(a.rewards, b.rewards, sizeof(double) * E));
     UT_CUDA(cp(a.dones, b.dones, (size_t)E));
@@ -657,6 +691,7 @@ int ut_vecenv_set_output_buffers(ut_vecenv* v, int n) {
 }
 
 int ut_vecenv_copy_outputs_async(ut_vecenv* v, const ut_host_outputs* d, void* cuda_stream) {
+  DeviceGuard dg(v->device);
   cudaStream_t cs = static_cast<cudaStream_t>(cuda_stream);
   if (!v->step_done) UT_CUDA(cudaEventCreateWithFlags(&v->step_done, cudaEventDisableTiming));
   cudaEvent_t& done = v->copy_done[v->cur];
@@ -685,6 +720,7 @@ int ut_vecenv_copy_outputs_async(ut_vecenv* v, const ut_host_outputs* d, void* c
 }
 
 int ut_vecenv_capture_trajectory(ut_vecenv* v, int64_t env_begin, int64_t env_end) {
+  DeviceGuard dg(v->device);
   if (env_begin < 0 || env_end > v->n_envs || env_begin > env_end)
     return fail(UT_ERR_CONTRACT, "capture_trajectory: env range [%lld, %lld) outside [0, %lld)",
                 (long long)env_begin, (long long)env_end, (long long)v->n_envs);
@@ -705,6 +741,7 @@ int ut_vecenv_capture_trajectory(ut_vecenv* v, int64_t env_begin, int64_t env_en
 }
 
 int ut_vecenv_trajectory_rows(ut_vecenv* v, double* rows, size_t cap, size_t* len) {
+  DeviceGuard dg(v->device);
   const size_t need = (size_t)((v->B.traj_hi - v->B.traj_lo) * v->R_max * kTrajFields);
   *len = need;
   if (!rows) return UT_OK;
@@ -716,6 +753,7 @@ int ut_vecenv_trajectory_rows(ut_vecenv* v, double* rows, size_t cap, size_t* le
 }
 
 int ut_vecenv_buffers(ut_vecenv* v, ut_buffers* o) {
+  DeviceGuard dg(v->device);
   const DevBatch& B = v->B;
   o->n_envs = v->n_envs;
   o->n_agents = v->A_max;
@@ -741,10 +779,13 @@ int ut_vecenv_buffers(ut_vecenv* v, ut_buffers* o) {
   o->vx = B.vx;
   o->vy = B.vy;
   o->w = B.w;
+  o->total_sets = v->total_sets;
+  o->set_offset = B.set_offset;
   return UT_OK;
 }
 
 int ut_vecenv_copy_outputs(ut_vecenv* v, const ut_host_outputs* d) {
+  DeviceGuard dg(v->device);
   const DevBatch& B = v->B;
   const int64_t n = v->n_envs, Am = v->A_max, Tm = v->T_max;
   auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
@@ -767,17 +808,32 @@ int ut_vecenv_copy_outputs(ut_vecenv* v, const ut_host_outputs* d) {
 }
 
 int ut_vecenv_set_stream(ut_vecenv* v, void* s) {
+  DeviceGuard dg(v->device);
   UT_CUDA(cudaStreamSynchronize(v->stream));
+  // NULL: the handle's own stream; UT_STREAM_LEGACY (== cudaStreamLegacy): the
+  // legacy default stream; anything else: a caller-owned cudaStream_t
   v->stream = s ? static_cast<cudaStream_t>(s) : v->own_stream;
   return UT_OK;
 }
 
+int ut_vecenv_wait_stream(ut_vecenv* v, void* s) {
+  DeviceGuard dg(v->device);
+  if (!v->order_ev) UT_CUDA(cudaEventCreateWithFlags(&v->order_ev, cudaEventDisableTiming));
+  const cudaStream_t cs = s ? static_cast<cudaStream_t>(s) : cudaStreamLegacy;
+  if (cs == v->stream) return UT_OK;
+  UT_CUDA(cudaEventRecord(v->order_ev, cs));
+  UT_CUDA(cudaStreamWaitEvent(v->stream, v->order_ev, 0));
+  return UT_OK;
+}
+
 int ut_vecenv_synchronize(ut_vecenv* v) {
+  DeviceGuard dg(v->device);
   UT_CUDA(cudaStreamSynchronize(v->stream));
   return UT_OK;
 }
 
 int ut_vecenv_stats(ut_vecenv* v, double out[UT_N_STATS], int reset) {
+  DeviceGuard dg(v->device);
   double* d;
   UT_CUDA(cudaMallocAsync((void**)&d, sizeof(double) * UT_N_STATS, v->stream));
   stats_kernel<<<1, 256, 0, v->stream>>>(v->B, d, reset);
@@ -792,31 +848,67 @@ int ut_vecenv_stats(ut_vecenv* v, double out[UT_N_STATS], int reset) {
 int64_t ut_vecenv_launch_count(const ut_vecenv* v) { return v->launches; }
 
 int ut_vecenv_enable_phase_timing(ut_vecenv* v, int on) {
+  DeviceGuard dg(v->device);
   UT_CUDA(cudaStreamSynchronize(v->stream));
   if (on && !v->phase_buf) {
     int rc;
-    if ((rc = v->alloc(&v->phase_buf, (size_t)v->grid * kPhaseCount))) return rc;
-    UT_CUDA(cudaMemset(v->phase_buf, 0, sizeof(unsigned long long) * v->grid * kPhaseCount));
+    if ((rc = v->alloc(&v->phase_buf, (size_t)v->grid * kPhaseSlots))) return rc;
+    UT_CUDA(cudaMemset(v->phase_buf, 0, sizeof(unsigned long long) * v->grid * kPhaseSlots));
   }
   v->B.phase_cycles = on ? v->phase_buf : nullptr;
   return v->sync_batch();
 }
 
 // Per-CTA phase cycles summed over the grid (each CTA steps a contiguous env
-// range, so this is the device analogue of the per-env phase sums).
-int ut_vecenv_phase_cycles(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset) {
-  for (int k = 0; k < UT_N_PHASES; ++k) out[k] = 0;
+// range, so this is the device analogue of the per-env phase sums), and the
+// same converted to ns with the SM-clock rate the CTAs saw (elapsed globaltimer
+// ns over elapsed cycles of every timed launch).
+namespace {
+int phase_sums(ut_vecenv* v, uint64_t cyc[UT_N_PHASES], double* ns_per_cycle, int reset) {
+  for (int k = 0; k < UT_N_PHASES; ++k) cyc[k] = 0;
+  *ns_per_cycle = 0.0;
   if (!v->phase_buf) return UT_OK;
   UT_CUDA(cudaStreamSynchronize(v->stream));
-  std::vector<unsigned long long> h((size_t)v->grid * kPhaseCount);
+  std::vector<unsigned long long> h((size_t)v->grid * kPhaseSlots);
   UT_CUDA(cudaMemcpy(h.data(), v->phase_buf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
-  for (size_t i = 0; i < h.size(); ++i) out[i % kPhaseCount] += h[i];
+  double c = 0.0, t = 0.0;
+  for (int b = 0; b < v->grid; ++b) {
+    const unsigned long long* r = h.data() + (size_t)b * kPhaseSlots;
+    for (int k = 0; k < kPhaseCount; ++k) cyc[k] += r[k];
+    c += (double)r[kPhaseWait + 1];
+    t += (double)r[kPhaseWait + 2];
+  }
+  *ns_per_cycle = c > 0.0 ? t / c : 0.0;
   if (reset) UT_CUDA(cudaMemset(v->phase_buf, 0, sizeof(unsigned long long) * h.size()));
   return UT_OK;
+}
+}  // namespace
+
+int ut_vecenv_phase_cycles(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset) {
+  DeviceGuard dg(v->device);
+  double r;
+  return phase_sums(v, out, &r, reset);
+}
+
+int ut_vecenv_phase_ns(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset) {
+  DeviceGuard dg(v->device);
+  double r;
+  uint64_t cyc[UT_N_PHASES];
+  const int rc = phase_sums(v, cyc, &r, reset);
+  for (int k = 0; k < UT_N_PHASES; ++k) out[k] = (uint64_t)std::llround((double)cyc[k] * r);
+  return rc;
+}
+
+int ut_vecenv_set_auto_reset(ut_vecenv* v, int on) {
+  DeviceGuard dg(v->device);
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  v->B.auto_reset = on ? 1 : 0;
+  return v->sync_batch();
 }
 
 // Environment::serialize_state (env.cpp:550-593)
 int ut_env_serialize(ut_vecenv* v, int64_t e, double* blob, size_t cap, size_t* len) {
+  DeviceGuard dg(v->device);
   if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "serialize: env %lld out of range", (long long)e);
   const DevConfig& d = v->cfg(e);
   const int A = d.A, T = d.T, P = d.P, sA = d.sA, sT = d.sT, AA = sA * sA, AT = sA * sT;
@@ -867,6 +959,7 @@ int ut_env_serialize(ut_vecenv* v, int64_t e, double* blob, size_t cap, size_t* 
 // Environment::deserialize_state (env.cpp:595-659). Like the reference, the batch
 // buffers are refreshed only by ut_vecenv_refresh_outputs().
 int ut_env_deserialize(ut_vecenv* v, int64_t e, const double* blob, size_t len) {
+  DeviceGuard dg(v->device);
   if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "deserialize: env %lld out of range", (long long)e);
   const DevConfig& d = v->cfg(e);
   const int A = d.A, T = d.T, P = d.P, sA = d.sA, sT = d.sT, AA = sA * sA, AT = sA * sT;
@@ -1021,6 +1114,7 @@ int blob_range(ut_vecenv* v, int64_t e_begin, int64_t e_end, size_t* total, cons
 }  // namespace
 
 int ut_vecenv_export_state(ut_vecenv* v, int64_t e_begin, int64_t e_end, double* blobs, size_t cap, size_t* len) {
+  DeviceGuard dg(v->device);
   size_t total = 0;
   int rc = blob_range(v, e_begin, e_end, &total, "export_state");
   if (rc) return rc;
@@ -1031,6 +1125,7 @@ int ut_vecenv_export_state(ut_vecenv* v, int64_t e_begin, int64_t e_end, double*
 }
 
 int ut_vecenv_import_state(ut_vecenv* v, int64_t e_begin, int64_t e_end, const double* blobs, size_t len) {
+  DeviceGuard dg(v->device);
   size_t total = 0;
   int rc = blob_range(v, e_begin, e_end, &total, "import_state");
   if (rc) return rc;
@@ -1040,6 +1135,7 @@ int ut_vecenv_import_state(ut_vecenv* v, int64_t e_begin, int64_t e_end, const d
 }
 
 int ut_env_world_step(ut_vecenv* v, int64_t e, int32_t* step) {
+  DeviceGuard dg(v->device);
   if (e < 0 || e >= v->n_envs) return fail(UT_ERR_CONTRACT, "world_step: env %lld out of range", (long long)e);
   double s = 0.0;
   UT_CUDA(cudaStreamSynchronize(v->stream));
@@ -1048,16 +1144,23 @@ int ut_env_world_step(ut_vecenv* v, int64_t e, int32_t* step) {
   return UT_OK;
 }
 
-// benchmark_sps (vecenv.cpp:175-202): warmup, then CUDA-event-timed steps.
+// benchmark_sps (vecenv.cpp:175-202): warmup, then CUDA-event-timed steps with
+// phase timing on (the reference times its phases in the same run).
 int ut_benchmark_sps(const ut_env_config* cfg, int64_t n_envs, int32_t n_steps, int policy, uint64_t seed,
                      int32_t warmup, int device, ut_benchmark_report* out) {
   ut_vecenv* v = nullptr;
   int rc = ut_vecenv_create(cfg, n_envs, seed, 0, device, &v);
   if (rc) return rc;
+  DeviceGuard dg(device);
   cudaEvent_t t0, t1;
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
   rc = ut_vecenv_step_policy(v, policy, warmup);
+  if (!rc) rc = ut_vecenv_enable_phase_timing(v, 1);
+  if (!rc) {
+    uint64_t scratch[UT_N_PHASES];
+    rc = ut_vecenv_phase_cycles(v, scratch, 1);
+  }
   if (!rc) {
     cudaEventRecord(t0, v->stream);
     rc = ut_vecenv_step_policy(v, policy, n_steps);
@@ -1076,6 +1179,9 @@ int ut_benchmark_sps(const ut_env_config* cfg, int64_t n_envs, int32_t n_steps, 
     out->wall_seconds = ms / 1e3;
     out->sps = (double)n_envs * n_steps / out->wall_seconds;
     out->agent_sps = out->sps * v->A_max;
+    rc = ut_vecenv_phase_ns(v, out->phase_ns, 0);
+    out->total_ns = 0;
+    for (int k = 0; k < UT_PHASE_RESET; ++k) out->total_ns += out->phase_ns[k];
   }
   ut_vecenv_destroy(v);
   return rc;
@@ -1169,20 +1275,28 @@ __global__ void __launch_bounds__(256) fp64_peak_kernel(int iters, double seed, 
 
 extern "C" {
 int ut_debug_set_knobs(ut_vecenv* v, int force_exact, int64_t trace_env) {
+  DeviceGuard dg(v->device);
   v->B.force_exact = force_exact;
   v->B.trace_env = trace_env;
   return v->sync_batch();
 }
+int ut_debug_instance(ut_vecenv* v, int32_t* full, int32_t* np) {
+  DeviceGuard dg(v->device);
+  *full = v->full ? 1 : 0;
+  *np = v->np;
+  return UT_OK;
+}
 int ut_debug_cta_cycles(ut_vecenv* v, uint64_t* out, int64_t cap, int64_t* n) {
+  DeviceGuard dg(v->device);
   *n = v->phase_buf ? (int64_t)v->grid : 0;
   if (!v->phase_buf || !out) return UT_OK;
   if (cap < *n) return fail(UT_ERR_CONTRACT, "cta_cycles: room for %lld CTAs, need %lld", (long long)cap, (long long)*n);
   UT_CUDA(cudaStreamSynchronize(v->stream));
-  std::vector<unsigned long long> h((size_t)v->grid * kPhaseCount);
+  std::vector<unsigned long long> h((size_t)v->grid * kPhaseSlots);
   UT_CUDA(cudaMemcpy(h.data(), v->phase_buf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
-  for (int64_t b = 0; b < *n; ++b) {
+  for (int64_t b = 0; b < *n; ++b) {  // busy cycles: every phase, not the grid-barrier waits
     uint64_t t = 0;
-    for (int k = 0; k < kPhaseCount; ++k) t += h[(size_t)b * kPhaseCount + k];
+    for (int k = 0; k < kPhaseCount; ++k) t += h[(size_t)b * kPhaseSlots + k];
     out[b] = t;
   }
   return UT_OK;

@@ -154,6 +154,35 @@ __device__ __forceinline__ int64_t set_off(const DevBatch& B, int64_t e) {
   return B.set_offset ? B.set_offset[e] : e * (int64_t)(B.cfgs[0].A * B.cfgs[0].T);
 }
 
+// Phase timing (PhaseTimer, env.cpp:18-36, enabled when B.phase_cycles is set):
+// thread 0 of the CTA closes the running section into phase k and opens the
+// next; the CTA's sums are flushed to B.phase_cycles at the end of the launch.
+__shared__ long long g_ph[kPhaseWait + 2];  // phases, barrier waits, last timestamp
+constexpr int kPhLast = kPhaseWait + 1;
+__device__ __forceinline__ void ph_mark(const DevBatch& B, int k) {
+  if (threadIdx.x == 0 && B.phase_cycles != nullptr) {
+    const long long now = clock64();
+    g_ph[k] += now - g_ph[kPhLast];
+    g_ph[kPhLast] = now;
+  }
+}
+// The same for a section that belongs to two phases in the ratio num : den - num.
+__device__ __forceinline__ void ph_mark_split(const DevBatch& B, int k1, int k2, int num, int den) {
+  if (threadIdx.x == 0 && B.phase_cycles != nullptr) {
+    const long long now = clock64();
+    const long long d = now - g_ph[kPhLast];
+    const long long d1 = den > 0 ? d * num / den : d;
+    g_ph[k1] += d1;
+    g_ph[k2] += d - d1;
+    g_ph[kPhLast] = now;
+  }
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ void load_tables(const Smem& S) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) S.tab_log[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
   for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x)
@@ -232,6 +261,7 @@ __device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B,
     TG(V_Y, t) += TG(V_SPEED, t) * c.dt * sin(h);
     TG(V_COUNTDOWN, t) -= 1.0;
   }
+  ph_mark(B, PH_TARGETS);
   // actions (VecEnv::step_policy vecenv.cpp:118-135 or the caller's) + move_agents
   // (env.cpp:306-316, step_vehicle kinematics.cpp:51-56). The bench stream is
   // separate from the env stream and every action depends only on the agent's
@@ -262,6 +292,7 @@ __device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B,
     AG(V_Y, a) += AG(V_SPEED, a) * c.dt * sin(h);
   }
   if (mode == MODE_RANDOM) rec[R_BENCH_POS] = (double)bench.pos;
+  ph_mark(B, PH_AGENTS);
   // measure_ranges (env.cpp:318-347): targets outer, agents inner
   for (int t = 0; t < T; ++t) {
     bool detected = false;
@@ -284,6 +315,7 @@ __device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B,
     }
     rec[c.o_miss + t] = detected ? 0.0 : rec[c.o_miss + t] + 1.0;
   }
+  ph_mark(B, PH_MEASURE);
   // exchange_comms decisions (env.cpp:365-383); AgentInfo ages first
   for (int r = 0; r < A; ++r)
     for (int s = 0; s < A; ++s) INFO(I_AGE, r * sA + s) += 1.0;
@@ -308,6 +340,7 @@ __device__ __noinline__ void env_prologue(const DevConfig& c, const DevBatch& B,
   rec[R_ENV_POS] = (double)rng.pos;
   rec[R_ENV_HAVE_SPARE] = rng.have_spare ? 1.0 : 0.0;
   rec[R_ENV_SPARE] = rng.spare;
+  ph_mark(B, PH_COMMS);
 }
 
 // compute_reward_and_info (env.cpp:473-505) + VecEnv bookkeeping
@@ -1109,6 +1142,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     s.vx[j] = s.vx[j] * f;
     s.vy[j] = s.vy[j] * f;
   }
+  ph_mark(B, PH_FILTER);
 
   // ---- range updates: own ping, then fused senders (env.cpp:356-360, 385-392)
   SETPROF(2);
@@ -1233,9 +1267,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         exact = true;
       }
     }
-    if (exact && tid == 0) S.bc[kBcStatExact] += 1.0;
   }
   if (exact && nm > 0) {
+    if (tid == 0) S.bc[kBcStatExact] += 1.0;
     __syncthreads();  // every thread holds its particles: S.pf becomes the staging area
 #pragma unroll
     for (int q = 0; q < PPT; ++q)
@@ -1252,6 +1286,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     __syncthreads();  // the staging area is reused by the resample
   }
   const bool fresh = nm > 0;
+  // the update pass: the own ping's share is filter_step, the senders' comms
+  ph_mark_split(B, PH_FILTER, PH_COMMS, nm > 0 && ml[0] == ti ? 1 : 0, nm);
 
   // ---- pf::maybe_resample (tracking.cpp:172-178). With no update this step the
   // weights are the ones last step's maybe_resample already vetted (ESS >= P/2),
@@ -1330,6 +1366,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     S.bc[kBcStatUpdates] += (double)nm;
     S.bc[kBcStatResamples] += resampled ? 1.0 : 0.0;
   }
+  ph_mark(B, PH_COMMS);  // maybe_resample + estimate (env.cpp:397-409)
   SETPROF(10);
 }
 
@@ -1490,17 +1527,13 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     for (int k = 0; k <= kSetProfSlots; ++k) g_sp_acc[k] = k == kSetProfSlots ? clock64() : 0;
 #endif
   // phase timing (thread 0, shared memory: nothing live in registers)
-  __shared__ long long ph_cyc[kPhaseCount + 1];
   const bool timing = B.phase_cycles != nullptr;
-  if (timing && threadIdx.x == 0)
-    for (int k = 0; k <= kPhaseCount; ++k) ph_cyc[k] = 0;
-  auto mark = [&](int k) {  // close phase k (k < 0: open the first)
-    if (timing && threadIdx.x == 0) {
-      const long long now = clock64();
-      if (k >= 0) ph_cyc[k] += now - ph_cyc[kPhaseCount];
-      ph_cyc[kPhaseCount] = now;
-    }
-  };
+  __shared__ long long ph_t0[2];  // launch start: SM clock, globaltimer
+  if (timing && threadIdx.x == 0) {
+    for (int k = 0; k <= kPhaseWait; ++k) g_ph[k] = 0;
+    g_ph[kPhLast] = ph_t0[0] = clock64();
+    ph_t0[1] = (long long)globaltimer_ns();
+  }
   // Three phases separated by grid-wide barriers (cooperative launch: every CTA
   // is resident): the env prologues of the CTA's static env range; the particle
   // filters, envs handed out one at a time by a global counter so the grid
@@ -1508,14 +1541,13 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
   // mean); then outputs and auto-resets of the static range.
   cg::grid_group grid = cg::this_grid();
   const int n = (int)B.n_envs;
-  mark(-1);
   // ---- 1. prologue, one env per thread
   for (int e0 = lo; e0 < hi; e0 += blockDim.x) {
     const int e = e0 + threadIdx.x;
     if (e < min(hi, e0 + (int)blockDim.x)) env_prologue(cfg_of(Bg, e), Bg, e, B.env_index_offset + e, mode);
   }
-  mark(PH_PROLOGUE);
   grid.sync();  // every env's ping schedule is in place
+  ph_mark(B, kPhaseWait);
   // ---- 2. particle sets, env by env from the work counter; the next env is
   // claimed at the start of the current one so its first set can be prefetched
   int* claim = reinterpret_cast<int*>(S.bc + kBcClaim);
@@ -1551,8 +1583,9 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     }
     e = en;
   }
-  mark(PH_FILTER);
+  ph_mark(B, PH_FILTER);
   grid.sync();  // every estimate is in place
+  ph_mark(B, kPhaseWait);
   if (blockIdx.x == 0 && threadIdx.x == 0) *B.work = 0;  // for the next launch
   for (int e0 = lo; e0 < hi; e0 += blockDim.x) {
     const int e1 = min(hi, e0 + (int)blockDim.x);
@@ -1562,13 +1595,15 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
       if (e < e1) S.flags[threadIdx.x] = env_epilogue(cfg_of(Bg, e), Bg, e) ? kChunkFlagDone : 0;
     }
     __syncthreads();
+    ph_mark(B, PH_REWARD);
     write_outputs(Bg, e0, e1, S.flags, 0, false);
-    write_outputs(Bg, e0, e1, S.flags, kChunkFlagDone, true);  // terminal obs of finished envs
-    mark(PH_OUTPUT);
+    // terminal obs of finished envs (VecEnv auto-reset only)
+    if (B.auto_reset) write_outputs(Bg, e0, e1, S.flags, kChunkFlagDone, true);
+    ph_mark(B, PH_OBSERVE);
     // ---- 4. auto-reset of finished envs (vecenv.cpp:106-112)
     bool any = false;
     for (int i = 0; i < (int)(e1 - e0); ++i) any |= (S.flags[i] & kChunkFlagDone) != 0;
-    if (any) {
+    if (any && B.auto_reset) {
       __syncthreads();
       const int e = e0 + threadIdx.x;
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagDone)) {
@@ -1583,10 +1618,14 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagSpawned)) B.step[e] = 0;
     }
     __syncthreads();
-    mark(PH_RESET);
+    ph_mark(B, PH_RESET);
   }
-  if (timing && threadIdx.x == 0)
-    for (int k = 0; k < kPhaseCount; ++k) B.phase_cycles[blockIdx.x * kPhaseCount + k] += (unsigned long long)ph_cyc[k];
+  if (timing && threadIdx.x == 0) {
+    unsigned long long* out = B.phase_cycles + (size_t)blockIdx.x * kPhaseSlots;
+    for (int k = 0; k <= kPhaseWait; ++k) out[k] += (unsigned long long)g_ph[k];
+    out[kPhaseWait + 1] += (unsigned long long)(clock64() - ph_t0[0]);
+    out[kPhaseWait + 2] += globaltimer_ns() - (unsigned long long)ph_t0[1];
+  }
 #ifdef UT_SET_PROFILE
   if (threadIdx.x == 0)
     for (int k = 0; k < kSetProfSlots; ++k) atomicAdd(&g_setprof[k], (unsigned long long)g_sp_acc[k]);

@@ -117,8 +117,13 @@ struct DevBatch {
   int32_t force_exact;
   int64_t trace_env;
   // Phase timing (PhaseTimer, env.cpp:18-36): SM cycles per CTA accumulated in
-  // [grid][kPhaseCount] when non-null.
+  // [grid][kPhaseSlots] when non-null (kPhaseCount phases, the grid-barrier
+  // waits, then the CTA's elapsed SM cycles and globaltimer ns, which convert
+  // cycles to ns).
   unsigned long long* phase_cycles;
+  // VecEnv auto-reset of finished envs (vecenv.cpp:106-112); 0 = the single
+  // Environment semantics (env.cpp:234-504: step never resets, done stays set)
+  int32_t auto_reset;
   // Trajectory capture (append_trajectory_rows, trajectory.cpp:13-66) for envs
   // [traj_lo, traj_hi): after every step, before auto-reset, env e writes R_max
   // rows of kTrajFields doubles at traj[((e - traj_lo) * R_max + row) * kTrajFields].
@@ -134,9 +139,15 @@ struct DevBatch {
 enum : int { TJ_STEP = 0, TJ_X, TJ_Y, TJ_Z, TJ_HEAD, TJ_HAS_EST, TJ_EST_X, TJ_EST_Y, TJ_ERR, TJ_REWARD,
              TJ_COLLISION, TJ_IS_TARGET, kTrajFields };
 
-// Device phases (the reference's seven StepPhase values, env.hpp:71-80, map onto
-// these: targets+agents+measure+comm decisions -> PROLOGUE, filter+comm updates
-// -> FILTER, observe+reward -> OUTPUT, and auto-reset -> RESET).
-enum : int { PH_PROLOGUE = 0, PH_FILTER, PH_OUTPUT, PH_RESET, kPhaseCount };
+// Device phases: the reference's seven StepPhase values (env.hpp:71-80,
+// env.cpp:250-279) plus the auto-reset the reference leaves untimed
+// (vecenv.cpp:140). The merged range-update pass of a set is split between
+// FILTER (its own ping) and COMMS (the fused senders' pings) in proportion.
+enum : int { PH_TARGETS = 0, PH_AGENTS, PH_MEASURE, PH_FILTER, PH_COMMS, PH_OBSERVE, PH_REWARD, PH_RESET,
+             kPhaseCount };
+// per-CTA slots of B.phase_cycles: the phases, the grid-barrier waits, then the
+// launch's elapsed SM cycles and globaltimer ns
+constexpr int kPhaseWait = kPhaseCount;
+constexpr int kPhaseSlots = kPhaseCount + 3;
 
 }  // namespace ut

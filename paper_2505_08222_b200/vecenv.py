@@ -186,6 +186,10 @@ class VecEnv:
         _check(self._lib.ut_vecenv_buffers(self._h, C.byref(self._b)))
         self._views = {}
         self._n_out = 1
+        self._set_offsets = None
+        if isinstance(cfg, (list, tuple)):  # ragged particle store (ut_buffers.set_offset)
+            sizes = np.array([cfg[f].n_agents * cfg[f].n_targets for f in fleet], np.int64)
+            self._set_offsets = np.concatenate([[0], np.cumsum(sizes)])
 
     # -- shape (vecenv.hpp:29-33)
     def n_envs(self) -> int:
@@ -222,9 +226,21 @@ class VecEnv:
         if self._n_out == 2:
             self._sync_buffers()
 
+    # -- stream ordering
+    def _order_after_caller(self):
+        """The next device work of this handle runs after everything torch has
+        already enqueued on its current stream (a GPU policy producing actions,
+        kernels still reading the zero-copy output views)."""
+        import sys
+        torch = sys.modules.get("torch")
+        if torch is not None and torch.cuda.is_available() and torch.cuda.is_initialized():
+            s = torch.cuda.current_stream(self.device).cuda_stream
+            _check(self._lib.ut_vecenv_wait_stream(self._h, C.c_void_p(s)))
+
     # -- stepping
     def reset_all(self):
         """vecenv.cpp:69-77."""
+        self._order_after_caller()
         _check(self._lib.ut_vecenv_reset_all(self._h))
         self._after_write()
 
@@ -238,6 +254,7 @@ class VecEnv:
                 if t.numel() != self.n_envs() * self.n_agents():
                     raise ContractViolation("vecenv step: wrong action count")
                 if t.is_cuda:
+                    self._order_after_caller()  # the producer of `actions` may still be running
                     _check(self._lib.ut_vecenv_step(self._h, C.c_void_p(t.data_ptr()), 1))
                     self._after_write()
                     return
@@ -247,6 +264,7 @@ class VecEnv:
         a = np.ascontiguousarray(actions, dtype=np.int32).reshape(-1)
         if a.size != self.n_envs() * self.n_agents():
             raise ContractViolation("vecenv step: wrong action count")
+        self._order_after_caller()
         _check(self._lib.ut_vecenv_step(self._h, C.c_void_p(a.ctypes.data), 0))
         self._after_write()
 
@@ -254,11 +272,13 @@ class VecEnv:
         """vecenv.cpp:118-143 (``n_steps`` > 1 runs back-to-back device steps)."""
         if policy not in _POLICIES:
             raise ContractViolation(f"unknown policy {policy!r}")
+        self._order_after_caller()
         _check(self._lib.ut_vecenv_step_policy(self._h, _POLICIES[policy], n_steps))
         self._after_write()
 
     def refresh_outputs(self):
         """vecenv.cpp:145-150."""
+        self._order_after_caller()
         _check(self._lib.ut_vecenv_refresh_outputs(self._h))
 
     # -- zero-copy device views (vecenv.hpp:51-62)
@@ -301,13 +321,18 @@ class VecEnv:
         }
 
     def particles(self):
-        """The SoA particle store: px, py, vx, vy, w each (sets, P)."""
-        n_sets = None
+        """The SoA particle store: px, py, vx, vy, w each (total_sets, P). Env e's
+        set (a, t) is row set_offset(e) + a * T_e + t."""
         P = self._b.n_particles
-        # homogeneous batches: sets = n_envs * A * T
-        n_sets = self._b.n_envs * self._b.n_agents * self._b.n_targets
+        n_sets = int(self._b.total_sets)
         return {k: self._view("pf_" + k, getattr(self._b, k), (n_sets, P), "<f8")
                 for k in ("px", "py", "vx", "vy", "w")}
+
+    def set_offset(self, env: int) -> int:
+        """First particle-set row of env `env` (ragged for mixed fleets)."""
+        if self._set_offsets is None:
+            return env * self.n_agents() * self.n_targets()
+        return int(self._set_offsets[env])
 
     def host_outputs(self, names=None):
         """Copies the batch buffers to host numpy arrays (one synchronous call)."""
@@ -415,23 +440,36 @@ class VecEnv:
         _check(self._lib.ut_vecenv_stats(self._h, out, int(reset)))
         return np.array(out[:])
 
-    PHASES = ("prologue", "filter", "output", "reset")
+    PHASES = _abi.PHASE_NAMES
 
     def enable_phase_timing(self, on: bool = True):
         """VecEnv::enable_phase_timing (vecenv.hpp:64) on the device."""
         _check(self._lib.ut_vecenv_enable_phase_timing(self._h, int(on)))
 
     def phase_cycles(self, reset: bool = False) -> dict:
-        """SM cycles per device phase summed over envs (VecEnv::phase_ns analogue)."""
+        """SM cycles per phase (the reference's seven + reset), CTA-summed."""
         out = (C.c_uint64 * len(self.PHASES))()
         _check(self._lib.ut_vecenv_phase_cycles(self._h, out, int(reset)))
         return dict(zip(self.PHASES, out[:]))
+
+    def phase_ns(self, reset: bool = False) -> dict:
+        """VecEnv::phase_ns (vecenv.cpp:160-173): ns per phase, CTA-summed."""
+        out = (C.c_uint64 * len(self.PHASES))()
+        _check(self._lib.ut_vecenv_phase_ns(self._h, out, int(reset)))
+        return dict(zip(self.PHASES, out[:]))
+
+    def set_auto_reset(self, on: bool):
+        """Auto-reset of finished envs (vecenv.cpp:106-112); off = Environment semantics."""
+        _check(self._lib.ut_vecenv_set_auto_reset(self._h, int(on)))
 
     def launch_count(self) -> int:
         return int(self._lib.ut_vecenv_launch_count(self._h))
 
     def set_stream(self, stream_ptr: int):
-        _check(self._lib.ut_vecenv_set_stream(self._h, C.c_void_p(stream_ptr)))
+        """Run on a caller's CUDA stream; 0 is the legacy default stream (torch's
+        default), passed to the library as UT_STREAM_LEGACY."""
+        s = stream_ptr if stream_ptr else _abi.UT_STREAM_LEGACY
+        _check(self._lib.ut_vecenv_set_stream(self._h, C.c_void_p(s)))
 
     def synchronize(self):
         _check(self._lib.ut_vecenv_synchronize(self._h))
@@ -451,20 +489,30 @@ class VecEnv:
 
 class Environment:
     """One environment (env.hpp:91-171): a VecEnv shard holding the single global
-    env ``env_index``, so its streams equal ``Environment(cfg, seed, env_index)``."""
+    env ``env_index``, so its streams equal ``Environment(cfg, seed, env_index)``.
+    Like the reference it never resets on its own (env.cpp:234-504): after the
+    terminal step the state stays terminal (done stays set) until ``reset()``."""
 
     def __init__(self, cfg: EnvConfig, seed: int, env_index: int = 0, device: int = 0):
         self._v = VecEnv(cfg, 1, seed, env_index_offset=env_index, device=device)
+        self._v.set_auto_reset(False)
         self._cfg = cfg
 
     def config(self):
         return self._cfg
 
     def reset(self):
+        """Environment::reset (env.cpp:153-233)."""
         self._v.reset_all()
 
     def step(self, actions):
-        self._v.step(np.asarray(actions, np.int32).reshape(1, -1))
+        """Environment::step (env.cpp:235-287); invalid actions raise
+        ContractViolation("step: invalid action ...") and change nothing."""
+        try:
+            self._v.step(np.asarray(actions, np.int32).reshape(1, -1))
+        except ContractViolation as exc:
+            msg = str(exc)
+            raise ContractViolation(msg.split(": ", 1)[1] if msg.startswith("env ") else msg) from None
         o = self._v.host_outputs(["rewards", "dones", "collision", "tracking_error", "min_agent_dist",
                                   "target_lost"])
         return {"reward": float(o["rewards"][0]), "done": bool(o["dones"][0]),
@@ -507,4 +555,5 @@ def benchmark_sps(cfg: EnvConfig, n_envs: int, n_steps: int, policy="random", se
                                   C.byref(rep)))
     return {"n_envs": rep.n_envs, "n_agents": rep.n_agents, "n_targets": rep.n_targets,
             "timed_steps": rep.timed_steps, "wall_seconds": rep.wall_seconds, "sps": rep.sps,
-            "agent_sps": rep.agent_sps}
+            "agent_sps": rep.agent_sps, "phase_ns": dict(zip(_abi.PHASE_NAMES, rep.phase_ns[:])),
+            "total_ns": rep.total_ns}

@@ -95,6 +95,13 @@ def ref_lib():
         lib.ref_philox_block.restype = None
         lib.ref_derive_key.argtypes = [U64, U64, U64, U64]
         lib.ref_derive_key.restype = U64
+        lib.ref_env_create.argtypes = [cfgp, U64, I64, C.POINTER(P)]
+        lib.ref_env_destroy.argtypes = [P]
+        lib.ref_env_destroy.restype = None
+        lib.ref_env_reset.argtypes = [P]
+        lib.ref_env_step.argtypes = [P, P, C.POINTER(C.c_double), C.POINTER(I32), C.POINTER(I32)]
+        lib.ref_env_serialize_one.argtypes = [P, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_size_t)]
+        lib.ref_env_observation.argtypes = [P, I32, C.POINTER(C.c_double)]
         _ref_lib = lib
     return _ref_lib
 
@@ -250,6 +257,51 @@ class RefVecEnv(_Base):
     def close(self):
         if getattr(self, "h", None):
             self.lib.ref_vecenv_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+
+class RefEnvironment:
+    """The reference's own single utrack::Environment (oracle/_ref): no
+    auto-reset (env.cpp:234-504)."""
+
+    def __init__(self, cfg, seed, env_index=0):
+        self.lib = ref_lib()
+        self.A, self.T, self.P = cfg.n_agents, cfg.n_targets, cfg.pf.n_particles
+        h = C.c_void_p()
+        self._check(self.lib.ref_env_create(C.byref(cfg), seed, env_index, C.byref(h)))
+        self.h = h
+
+    def _check(self, rc):
+        if rc:
+            raise OracleError(rc, self.lib.ref_last_error().decode())
+
+    def step(self, actions):
+        a = np.ascontiguousarray(actions, np.int32)
+        r, d, c = C.c_double(), C.c_int32(), C.c_int32()
+        self._check(self.lib.ref_env_step(self.h, a.ctypes.data, C.byref(r), C.byref(d), C.byref(c)))
+        return {"reward": r.value, "done": bool(d.value), "collision": bool(c.value)}
+
+    def reset(self):
+        self._check(self.lib.ref_env_reset(self.h))
+
+    def serialize(self):
+        n = blob_len(self.A, self.T, self.P)
+        buf = np.zeros(n, np.float64)
+        ln = C.c_size_t()
+        self._check(self.lib.ref_env_serialize_one(self.h, buf.ctypes.data_as(C.POINTER(C.c_double)), n,
+                                                   C.byref(ln)))
+        return buf
+
+    def observation(self, agent):
+        out = np.zeros((self.A + self.T, UT_FEATURE_DIM), np.float64)
+        self._check(self.lib.ref_env_observation(self.h, agent, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.ref_env_destroy(self.h)
             self.h = None
 
     __del__ = close

@@ -56,11 +56,48 @@ def blob_spec(A, T, P):
     return np.array(names), np.array(ints, bool)
 
 
-def rel_err(a, b):
+# Relative comparison with a per-field absolute floor: |a - b| / max(|b|, floor).
+# A floor is where a value stops being meaningful relative to its own
+# magnitude: the rounding noise of the quantities it is computed from (machine
+# epsilon x their magnitude) divided by the tight tolerance. Positions,
+# estimates, spreads and distances are built from coordinates of up to ~1 km
+# (noise ~1e-13 m), so below 1 mm (1e-3 m) they are held to 1e-12 m absolute and
+# above it relatively. The spread is a root-mean-square over P particles of
+# differences of such coordinates, so its noise is up to ~P eps |x| ~ 1e-10 m:
+# floor 1 cm (a collapsed cloud has spread 0 on one side and ~1e-11 m of
+# rounding noise on the other). Headings, speeds, velocities, rewards and
+# normals (inputs of order 1) use 1e-6; the token columns scale metres by 1/1000
+# (floor 1e-6) and the spread by 1/100 (1e-4); the particle weights (~1/P) use
+# 1e-12 / P, so a weight of 1e-300 is held to 1e-21 absolute.
+DEFAULT_FLOOR = 1e-6
+METRE_FLOOR = 1e-3
+SPREAD_FLOOR = 1e-2
+METRE_GROUPS = ("agent.x", "agent.y", "agent.z", "target.x", "target.y", "target.z", "info.x", "info.y",
+                "info.z", "track.est_x", "track.est_y", "pf.px", "pf.py")
+OUTPUT_FLOORS = {"tracking_error": METRE_FLOOR, "min_agent_dist": METRE_FLOOR}
+# obs / final_obs columns (env_config.hpp:15-34): dx dy dz sin cos speed self agent
+# target valid age spread
+OBS_COL_FLOORS = np.array([1e-6] * 11 + [SPREAD_FLOOR / 100])
+
+
+def weight_floor(P):
+    return 1e-12 / max(int(P), 1)
+
+
+def blob_floors(names, P):
+    """Per-slot floors for the float slots `names` of a state blob."""
+    f = np.full(names.shape, DEFAULT_FLOOR)
+    f[np.isin(names, METRE_GROUPS)] = METRE_FLOOR
+    f[names == "track.spread"] = SPREAD_FLOOR
+    f[names == "pf.w"] = weight_floor(P)
+    return f
+
+
+def rel_err(a, b, floor=DEFAULT_FLOOR):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     d = np.abs(a - b)
-    scale = np.maximum(np.abs(b), 1.0)
+    scale = np.maximum(np.abs(b), floor)
     with np.errstate(invalid="ignore"):
         r = np.where(d == 0, 0.0, d / scale)
     return r
@@ -90,12 +127,18 @@ def compare_blobs(got, want, A, T, P, report=None, tag=""):
     for i in bad[:20]:
         rep.int_mismatch.append((tag, names[i], int(i), float(got[i]), float(want[i])))
     fl = ~ints
-    r = rel_err(got[fl], want[fl])
+    r = rel_err(got[fl], want[fl], blob_floors(names[fl], P))
     for g in np.unique(names[fl]):
         m = names[fl] == g
         v = float(r[m].max()) if m.any() else 0.0
         rep.max_rel[g] = max(rep.max_rel.get(g, 0.0), v)
     return rep
+
+
+def output_floor(name, arr):
+    if name in ("obs", "final_obs"):
+        return OBS_COL_FLOORS.reshape(12, 1) if np.ndim(arr) == 2 else DEFAULT_FLOOR
+    return OUTPUT_FLOORS.get(name, DEFAULT_FLOOR)
 
 
 INT_OUTPUTS = ("dones", "masks", "target_lost", "collision", "step")
@@ -111,6 +154,6 @@ def compare_outputs(got, want, report=None, tag="", skip=()):
                 rep.int_mismatch.append((tag, k, idx[:5].tolist()))
     for k in FLOAT_OUTPUTS:
         if k in got and k in want and k not in skip:
-            r = rel_err(got[k], want[k])
+            r = rel_err(got[k], want[k], output_floor(k, want[k]))
             rep.max_rel["out." + k] = max(rep.max_rel.get("out." + k, 0.0), float(r.max()) if r.size else 0.0)
     return rep
