@@ -2,13 +2,19 @@
 """Throughput of the batched JaxLrauv environment step on B200.
 
 Metric (BASELINE.json): agent-env steps/sec on the 5-agent / 5-fast-target
-workload (65,536 envs per GPU, P = 1024, fp64 particle
-filters), random legal actions from the device bench stream (vecenv.cpp:118-135).
-Multi-GPU (torchrun): envs shard by global index range, each GPU steps its
-shard independently (weak scaling, no data-path collective); the episode
-statistics are all-reduced once over NCCL after the run.
+workload (65,536 envs, P = 1024, fp64 particle filters),
+random legal actions from the device bench stream (vecenv.cpp:118-135).
+
+Multi-GPU: one process per GPU. Under torchrun the ranks come from the
+environment; `--gpus N` without WORLD_SIZE re-launches itself under
+torch.distributed.run with N processes. Envs shard by global index range and
+each GPU steps its shard independently (no data-path collective); the episode
+statistics are all-reduced once over NCCL after the run (NCCL_DEBUG=INFO).
+C3 (and C1/C2) scale strongly -- 65,536 envs in total, 8,192 per GPU at N = 8
+(SURVEY §8e); C4/C5 weakly (their per-GPU shard is fixed by HBM capacity).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+                  [--scaling strong|weak] [--dry-run]
 """
 import argparse
 import json
@@ -40,6 +46,9 @@ CONFIGS = {
                n_agents=8, n_targets=8, spawn_max_sep=600.0, horizon=128, envs=65536, mix=True),
 }
 MIX_TAG = 0x6d6978  # "mix"
+# C3 is the strong-scaling workload (67 GB fits one GPU); C5 needs
+# 135 GB per GPU even at N = 8 and C4 ~218 GB ragged, so they scale weakly.
+DEFAULT_SCALING = {"c1": "strong", "c2": "strong", "c3": "strong", "c4": "weak", "c5": "weak"}
 
 
 def mix_fleet(lo, hi, seed=0):
@@ -147,25 +156,38 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def workload_config(name, per_gpu, total, particles):
+def workload_config(name, per_gpu, total, particles, scaling):
     """The `config` object both arms print (same workload, same keys)."""
     c = CONFIGS[name]
     A, T = c["n_agents"], c["n_targets"]
     gb = algorithmic_bytes_per_env_step(A, T, particles, rec_words_for(A, T)) * per_gpu / 1e9
     return {"workload": f"{name}: {c['desc']}", "envs_per_gpu": per_gpu, "total_envs": total,
-            "particles": particles, "agents": A, "targets": T,
+            "particles": particles, "agents": A, "targets": T, "horizon": c["horizon"], "scaling": scaling,
             "policy": "random legal (bench stream, vecenv.cpp:125-134)",
             "l2": f"inputs larger than L2 ({gb:.1f} GB touched per step per GPU)"}
 
 
-def measured_traffic(name, per_gpu, particles):
-    """DRAM bytes per step-kernel launch from the committed ncu --set full capture
-    of the same workload (profiles/traffic.json), or None."""
+def shard_plan(name, world, rank, args):
+    """(scaling, per-GPU envs nominal, total envs, this rank's [lo, hi))."""
+    from paper_2505_08222_b200.sharding import shard_range
+    scaling = args.scaling or DEFAULT_SCALING[name]
+    if scaling == "strong":
+        total = args.total_envs or CONFIGS[name]["envs"]
+        per_gpu = -(-total // world)
+    else:
+        per_gpu = args.envs_per_gpu or CONFIGS[name]["envs"]
+        total = per_gpu * world
+    lo, hi = shard_range(total, rank, world)
+    return scaling, per_gpu, total, lo, hi
+
+
+def measured_counts(name, per_gpu, particles):
+    """ncu counters per step-kernel launch of the same workload (profiles/traffic.json,
+    from `ncu --metrics ...` captures): DRAM bytes, fp64 thread instructions."""
     p = ROOT / "profiles" / "traffic.json"
     if not p.exists():
-        return None
-    d = json.loads(p.read_text()).get(f"{name}:{per_gpu}:{particles}")
-    return None if d is None else float(d["dram_bytes_per_launch"])
+        return {}
+    return json.loads(p.read_text()).get(f"{name}:{per_gpu}:{particles}", {})
 
 
 def measured_peaks():
@@ -186,6 +208,12 @@ def fp64_peak_per_s(device):
     if lib.ut_debug_fp64_peak(device, C.byref(out)) != 0:
         return None
     return out.value
+
+
+REF_BUILD = ("reference sources compiled unmodified by oracle/Makefile: -O3 -std=gnu++20 -march=x86-64-v3 "
+             "-ffp-contract=off (reference: -march=native, contraction on); Eigen 3.4 is absent here, so a "
+             "shim supplies it with correctly rounded fp32 log/sin/cos through libm and sequential reductions "
+             "(Eigen: SIMD polynomials) -- a slower CPU path than a real-Eigen -march=native build")
 
 
 def cpu_baseline(cfg_name, particles, budget_s=12.0):
@@ -227,10 +255,17 @@ def cpu_baseline(cfg_name, particles, budget_s=12.0):
     steps = int(max(2, min(64, budget_s / max(wall, 1e-3))))
     sps, wall, wk, ph = run(steps, 2)
     names = ["targets", "agents", "measure", "filter", "comms", "observe", "reward"]
-    return {"value": sps * A, "unit": "agent-env steps/s", "cores": wk, "kind": kind,
-            "sample": f"{n_envs} envs x {steps} steps of {cfg_name} (P={particles}), "
-                      f"benchmark_sps(kRandom) after 2 warmup steps, {wall:.1f} s wall",
-            "env_sps": sps, "phase_ns": dict(zip(names, ph)) if ph else None}
+    out = {"value": sps * A, "unit": "agent-env steps/s", "cores": wk, "kind": kind,
+           "sample": f"{n_envs} envs x {steps} steps of {cfg_name} (P={particles}), "
+                     f"benchmark_sps(kRandom) after 2 warmup steps, {wall:.1f} s wall",
+           "timed_envs": n_envs, "timed_steps": steps, "env_sps": sps,
+           "build": REF_BUILD if kind == "reference" else "oracle/ut_oracle.c restatement, 1 thread"}
+    if ph:
+        tot = float(sum(ph)) or 1.0
+        out["phase_ns"] = dict(zip(names, ph))
+        out["phase_ns_per_env_step"] = {k: v / (n_envs * steps) for k, v in zip(names, ph)}
+        out["phase_share"] = {k: v / tot for k, v in zip(names, ph)}
+    return out
 
 
 def run_reference_arm(args):
@@ -238,18 +273,82 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     base = cpu_baseline(args.config, args.particles, budget_s=max(5.0, 2.0 * (args.steps + args.warmup)))
-    per_gpu = args.envs_per_gpu or CONFIGS[args.config]["envs"]
+    scaling = args.scaling or DEFAULT_SCALING[args.config]
+    world = max(1, args.gpus)
+    if scaling == "strong":
+        total = args.total_envs or CONFIGS[args.config]["envs"]
+        per_gpu = -(-total // world)
+    else:
+        per_gpu = args.envs_per_gpu or CONFIGS[args.config]["envs"]
+        total = per_gpu * world
+    config = workload_config(args.config, per_gpu, total, args.particles, scaling)
+    config["timed_envs"] = base["timed_envs"]
+    config["note"] = (f"the CPU reference timed {base['timed_envs']} envs (host RAM: ~2.9 MB per 5v5 env), "
+                      "not the full batch; SPS is flat in n_envs once n_envs >> cores (SPEC.md:426)")
     line = {
-        "metric": "agent-env steps/sec (5v5 fast targets)" if args.config == "c3" else f"agent-env steps/sec ({args.config})",
+        "metric": metric_name(args.config),
         "value": base["value"], "unit": "agent-env steps/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args.config, per_gpu, per_gpu * args.gpus, args.particles),
-        "cpu_baseline": base,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config, "cpu_baseline": base,
         "e2e": {"value": base["value"], "unit": "agent-env steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def metric_name(name):
+    return "agent-env steps/sec (5v5 fast targets)" if name == "c3" else f"agent-env steps/sec ({name})"
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_ranks(n):
+    """`--gpus N` outside torchrun: re-launch this script as N ranks, exactly like
+    the driver does (torch.distributed.run, rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(pathlib.Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, cwd=str(ROOT))
+
+
+def dry_run(args):
+    """The multi-rank plumbing without stepping: process group (NCCL on GPUs, gloo
+    without), shard ranges, a MAX and a SUM all-reduce; rank 0 prints one line."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    use_cuda = torch.cuda.is_available()
+    if world > 1:
+        if use_cuda:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl" if use_cuda else "gloo")
+    scaling, per_gpu, total, lo, hi = shard_plan(args.config, world, rank, args)
+    dev = "cuda" if use_cuda else "cpu"
+    rng = torch.tensor([float(lo), float(hi)], dtype=torch.float64, device=dev)
+    ranges = [torch.zeros_like(rng) for _ in range(world)]
+    cnt = torch.tensor([float(hi - lo)], dtype=torch.float64, device=dev)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_gather(ranges, rng)
+        dist.all_reduce(cnt)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    else:
+        ranges = [rng]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": scaling, "total_envs": total,
+                          "envs_per_gpu": per_gpu, "backend": dist.get_backend() if world > 1 else None,
+                          "ranges": [[int(a), int(b)] for a, b in (r.tolist() for r in ranges)],
+                          "envs_sum": int(cnt.item()), "max_rank": int(t.item())}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -259,16 +358,23 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default=None, choices=["strong", "weak"],
+                    help="strong: --total-envs over all GPUs; weak: --envs-per-gpu on each (default per config)")
     ap.add_argument("--envs-per-gpu", type=int, default=None)
+    ap.add_argument("--total-envs", type=int, default=None)
     ap.add_argument("--particles", type=int, default=1024)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--traffic-bytes", type=float, default=None,
-                    help="dram bytes per launch from an ncu --set full capture (profiles/)")
+    ap.add_argument("--no-episode", action="store_true", help="skip the full-horizon / reset-step timing")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only (no stepping)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.dry_run:
+        return dry_run(args)
 
     import numpy as np
     import torch
@@ -279,16 +385,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2505_08222_b200.vecenv import VecEnv
-    from paper_2505_08222_b200.sharding import shard_range
     from paper_2505_08222_b200._abi import STAT_NAMES
 
     cfg = make_cfg(args.config, args.particles)
     A, T, P = cfg.n_agents, cfg.n_targets, cfg.pf.n_particles
-    per_gpu = args.envs_per_gpu or CONFIGS[args.config]["envs"]
-    total = per_gpu * world
-    lo, hi = shard_range(total, rank, world)
+    scaling, per_gpu, total, lo, hi = shard_plan(args.config, world, rank, args)
     if CONFIGS[args.config].get("mix"):
         fleets = mix_fleet(lo, hi)
         shapes = [(a, t) for a in range(1, 9) for t in range(1, 9)]
@@ -302,7 +406,7 @@ def main():
         agents_local = (hi - lo) * A
         pf_bytes_local = (hi - lo) * 80 * P * A * T
     stream = torch.cuda.current_stream()
-    venv.set_stream(stream.cuda_stream)
+    venv.set_stream(stream.cuda_stream)  # the legacy default stream: the events below bracket the kernels
 
     venv.step_policy("random", args.warmup)
     torch.cuda.synchronize()
@@ -321,21 +425,30 @@ def main():
         if prev is not None and abs(t_one - prev) <= 0.03 * prev:
             break
         prev = t_one
+    # windows of exactly K steps; short ones are repeated until ~1 s has been
+    # timed so the clock sampler (200 ms period) sees the load (median window)
+    windows = max(1, min(50, int(1000.0 / max(prev or t_one, 1e-3) / max(1, args.steps)) + 1))
     if world > 1:
-        dist.barrier()
+        t_w = torch.tensor([windows], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t_w, op=dist.ReduceOp.MAX)
+        windows = int(t_w.item())
     launches0 = venv.launch_count()
     upd0 = float(venv.stats()[STAT_NAMES.index("pf_updates")])
+    times = []
     with ClockSampler(local) as clocks:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        start.record(stream)
-        venv.step_policy("random", args.steps)
-        end.record(stream)
-        torch.cuda.synchronize()
-    gpu_launches = venv.launch_count() - launches0
-    upd_timed = float(venv.stats()[STAT_NAMES.index("pf_updates")]) - upd0
-    ms = start.elapsed_time(end)
+        for _ in range(windows):
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            start.record(stream)
+            venv.step_policy("random", args.steps)
+            end.record(stream)
+            torch.cuda.synchronize()
+            times.append(start.elapsed_time(end))
+    gpu_launches = (venv.launch_count() - launches0) // windows
+    upd_timed = (float(venv.stats()[STAT_NAMES.index("pf_updates")]) - upd0) / windows
+    ms = statistics.median(times)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -348,6 +461,58 @@ def main():
     agents_total = float(ag.item())  # = total * A for a homogeneous fleet
     value = agents_total * args.steps / secs
 
+    # ---- one full horizon (auto-reset included: every env finishes once), then
+    # the reset step alone, with the device phase timers on around it
+    episode = None
+    if not args.no_episode:
+        horizon = CONFIGS[args.config]["horizon"]
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        start.record(stream)
+        venv.step_policy("random", horizon)
+        end.record(stream)
+        torch.cuda.synchronize()
+        ep_ms = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ep_ms, op=dist.ReduceOp.MAX)
+        ep_ms = float(ep_ms.item())
+        # align to the step before the (aligned) auto-reset
+        k = venv.world_step(0)
+        if k < horizon - 2:
+            venv.step_policy("random", horizon - 2 - k)
+        elif k == horizon - 1:
+            venv.step_policy("random", horizon - 1)
+        venv.enable_phase_timing(True)
+        venv.phase_ns(reset=True)
+        step_ms, phases = [], []
+        for _ in range(3):  # before, reset, after
+            torch.cuda.synchronize()
+            start.record(stream)
+            venv.step_policy("random", 1)
+            end.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(start.elapsed_time(end))
+            phases.append(venv.phase_ns(reset=True))
+        venv.enable_phase_timing(False)
+        names7 = ("targets", "agents", "measure", "filter", "comms", "observe", "reward")
+        n_loc = hi - lo
+        plain = {k: (phases[0][k] + phases[2][k]) / 2.0 for k in names7}
+        tot7 = sum(plain.values()) or 1.0
+        episode = {
+            "steps": horizon, "ms": ep_ms, "ms_per_step": ep_ms / horizon,
+            "value": agents_total * horizon / (ep_ms / 1e3),
+            "reset_step_ms": step_ms[1], "step_ms_before_after_reset": [step_ms[0], step_ms[2]],
+            "reset_over_step": step_ms[1] / (0.5 * (step_ms[0] + step_ms[2])),
+            "note": "one horizon of steps timed as one window: every env auto-resets once inside it "
+                    "(vecenv.cpp:140); `value` above is the K-step window the driver asks for",
+            "phase_ns_per_env_step": {k: v / n_loc for k, v in plain.items()},
+            "phase_share": {k: v / tot7 for k, v in plain.items()},
+            "reset_ns_per_env": phases[1]["reset"] / n_loc,
+            "phase_timer": "SM clock of thread 0 per CTA, CTA-summed, ns at the measured clock "
+                           "(UT_PHASE_*, ut_env.h); shares comparable to cpu_baseline.phase_share",
+        }
+
     # episode statistics: the one NCCL collective (north_star)
     st = torch.tensor(venv.stats(), dtype=torch.float64, device="cuda")
     if world > 1:
@@ -357,16 +522,17 @@ def main():
     # ---- e2e through the public API with host buffers (pinned), copies timed
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 10)
     n_loc = hi - lo
-    acts_h = torch.empty((n_loc, A), dtype=torch.int32, pin_memory=True)
+    Am, Rm, Tm = venv.n_agents(), venv.n_rows(), venv.n_targets()
+    acts_h = torch.empty((n_loc, Am), dtype=torch.int32, pin_memory=True)
     host = {
-        "obs": torch.empty((12, n_loc * A * (A + T)), dtype=torch.float64, pin_memory=True),
-        "global_state": torch.empty((12, n_loc * (A + T)), dtype=torch.float64, pin_memory=True),
+        "obs": torch.empty((12, n_loc * Am * Rm), dtype=torch.float64, pin_memory=True),
+        "global_state": torch.empty((12, n_loc * Rm), dtype=torch.float64, pin_memory=True),
         "rewards": torch.empty(n_loc, dtype=torch.float64, pin_memory=True),
         "dones": torch.empty(n_loc, dtype=torch.uint8, pin_memory=True),
-        "masks": torch.empty(n_loc * A * 5, dtype=torch.uint8, pin_memory=True),
-        "tracking_error": torch.empty(n_loc * T, dtype=torch.float64, pin_memory=True),
-        "min_agent_dist": torch.empty(n_loc * T, dtype=torch.float64, pin_memory=True),
-        "target_lost": torch.empty(n_loc * T, dtype=torch.uint8, pin_memory=True),
+        "masks": torch.empty(n_loc * Am * 5, dtype=torch.uint8, pin_memory=True),
+        "tracking_error": torch.empty(n_loc * Tm, dtype=torch.float64, pin_memory=True),
+        "min_agent_dist": torch.empty(n_loc * Tm, dtype=torch.float64, pin_memory=True),
+        "target_lost": torch.empty(n_loc * Tm, dtype=torch.uint8, pin_memory=True),
         "collision": torch.empty(n_loc, dtype=torch.uint8, pin_memory=True),
     }
     d2h = sum(v.numel() * v.element_size() for v in host.values())
@@ -382,7 +548,8 @@ def main():
     acts_np = acts_h.numpy().reshape(-1)
     # host policy: a uniform legal action per agent from its returned 5-bit mask
     # (lookup of the j-th set bit, j = floor(u * #legal)), vectorised with
-    # preallocated buffers and 1-D takes
+    # preallocated buffers and 1-D takes; padding agents of mixed fleets have
+    # no legal action and get 0 (ignored by the step)
     kth = np.zeros((32, 5), np.int32)
     n_legal = np.zeros(32, np.float32)
     for code in range(32):
@@ -390,7 +557,7 @@ def main():
         n_legal[code] = len(bits)
         kth[code, :len(bits)] = bits
     kth_flat = kth.reshape(-1)
-    n_ag = n_loc * A
+    n_ag = n_loc * Am
     u = np.empty(n_ag, np.float32)
     code = np.empty(n_ag, np.uint8)
     tmp = np.empty(n_ag, np.uint8)
@@ -420,36 +587,41 @@ def main():
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = agents_total * e2e_steps / float(te.item())
+    e2e_value = agents_total * e2e_steps / float(te.item()) if e2e_steps else None
 
     peak, peak_kind = measured_peaks()
     # particle bytes of this shard's fleet + record and (padded) outputs per env
     per_env_rest = algorithmic_bytes_per_env_step(A, T, P, rec_words_for(A, T)) - 80 * P * A * T
     bytes_launch = pf_bytes_local + per_env_rest * (hi - lo)
-    avg_launch_s = secs / max(1, args.steps)
+    avg_launch_s = ms / 1e3 / max(1, args.steps)  # this rank's own launches
     achieved = bytes_launch / avg_launch_s / 1e9
-    # SURVEY 8d fp64 component: 39 + 55 u algorithmic fp64 instructions per
-    # particle per step (u = range updates applied to its set this step, counted
-    # by the kernel), against the device's measured DFMA issue rate.
-    sets_local = pf_bytes_local // (80 * P)
-    fp64_launch = P * (39.0 * sets_local * args.steps + 55.0 * upd_timed) / args.steps
+    counts = measured_counts(args.config, hi - lo, P)
     fp64_peak = fp64_peak_per_s(local)
+    sets_local = pf_bytes_local // (80 * P)
+    if counts.get("fp64_thread_inst_per_launch"):
+        fp64_launch = float(counts["fp64_thread_inst_per_launch"])
+        fp64_src = counts.get("fp64_source", "ncu smsp__sass_thread_inst_executed_op_d{fma,mul,add}_pred_on.sum")
+    else:  # SURVEY 8d model: 39 + 55 u fp64 instructions per particle-step
+        fp64_launch = P * (39.0 * sets_local + 55.0 * upd_timed / max(1, args.steps))
+        fp64_src = "model 39 + 55 u per particle-step (SURVEY 8d): no ncu counts for this workload"
     fp64_achieved = fp64_launch / avg_launch_s
 
     line = {
-        "metric": "agent-env steps/sec (5v5 fast targets)" if args.config == "c3" else f"agent-env steps/sec ({args.config})",
+        "metric": metric_name(args.config),
         "value": value, "unit": "agent-env steps/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_config(args.config, per_gpu, total, P), env_steps_per_s=env_steps / secs,
-                       settle_steps=settle_steps),
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(workload_config(args.config, per_gpu, total, P, scaling), env_steps_per_s=env_steps / secs,
+                       settle_steps=settle_steps, timed_windows=windows,
+                       window_ms=[round(x, 4) for x in times]),
         "e2e": {"value": e2e_value, "unit": "agent-env steps/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                "path": "VecEnv.step(host int32 actions from a host policy on the returned masks) + every output to pinned host (ut_vecenv_step, ut_vecenv_copy_outputs for the masks, ut_vecenv_copy_outputs_async for the rest, overlapping the next step)"},
+                "path": "VecEnv.step(host int32 actions from a host policy on the returned masks) + every output "
+                        "to pinned host (ut_vecenv_step, ut_vecenv_copy_outputs for the masks, "
+                        "ut_vecenv_copy_outputs_async for the rest, overlapping the next step)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
-                     "traffic": args.traffic_bytes if args.traffic_bytes is not None
-                     else measured_traffic(args.config, per_gpu, P),
+                     "traffic": counts.get("dram_bytes_per_launch"),
                      "kernel": "step_kernel<4,1024,FULL>", "bytes_per_launch": bytes_launch,
                      "avg_launch_ms": avg_launch_s * 1e3, "peak_source": peak_kind,
                      "components": {
@@ -457,14 +629,15 @@ def main():
                          "fp64": {"achieved_tinstr_s": fp64_achieved / 1e12,
                                   "peak_tinstr_s": fp64_peak / 1e12 if fp64_peak else None,
                                   "frac": fp64_achieved / fp64_peak if fp64_peak else None,
-                                  "instr_per_launch": fp64_launch,
+                                  "instr_per_launch": fp64_launch, "source": fp64_src,
                                   "updates_per_set_step": upd_timed / max(1, sets_local * args.steps),
-                                  "model": "39 + 55 u fp64 instr per particle-step (SURVEY 8d)",
                                   "peak_source": "ut_debug_fp64_peak (8 DFMA chains/thread)"}}},
         "gpu_launches": gpu_launches,
         "clocks": clocks.summary(),
         "stats": {k: float(v) for k, v in zip(STAT_NAMES, st)},
     }
+    if episode is not None:
+        line["episode"] = episode
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(args.config, P)

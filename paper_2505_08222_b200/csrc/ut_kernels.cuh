@@ -93,6 +93,12 @@ struct FixedSmem {
   double bc[16];
   uint4 xch[32 * 5];
   uint64_t mbar[2];
+  // phase timers (thread 0): the phases, barrier waits, the running section's
+  // start, and the launch's start clock / globaltimer. Kept in the dynamic
+  // block like everything else: the kernels share out-of-line device functions
+  // that address shared memory at fixed offsets, so no kernel may add static
+  // shared variables in front of the dynamic block.
+  long long ph[kPhaseWait + 4];
   // one particle set: the TMA landing zone of the set being read, then (once
   // every thread holds its particles) the staging of the exact update and the
   // resample, and in the reset phase the re-init words
@@ -157,10 +163,14 @@ __device__ __forceinline__ int64_t set_off(const DevBatch& B, int64_t e) {
 // Phase timing (PhaseTimer, env.cpp:18-36, enabled when B.phase_cycles is set):
 // thread 0 of the CTA closes the running section into phase k and opens the
 // next; the CTA's sums are flushed to B.phase_cycles at the end of the launch.
-__shared__ long long g_ph[kPhaseWait + 2];  // phases, barrier waits, last timestamp
-constexpr int kPhLast = kPhaseWait + 1;
+constexpr int kPhLast = kPhaseWait + 1;  // Smem::ph slots: running section start, then launch start clock / ns
+__device__ __forceinline__ long long* ph_slots() {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  return reinterpret_cast<FixedSmem<256>*>(smem_raw)->ph;  // offset independent of NP (precedes pf)
+}
 __device__ __forceinline__ void ph_mark(const DevBatch& B, int k) {
   if (threadIdx.x == 0 && B.phase_cycles != nullptr) {
+    long long* g_ph = ph_slots();
     const long long now = clock64();
     g_ph[k] += now - g_ph[kPhLast];
     g_ph[kPhLast] = now;
@@ -169,6 +179,7 @@ __device__ __forceinline__ void ph_mark(const DevBatch& B, int k) {
 // The same for a section that belongs to two phases in the ratio num : den - num.
 __device__ __forceinline__ void ph_mark_split(const DevBatch& B, int k1, int k2, int num, int den) {
   if (threadIdx.x == 0 && B.phase_cycles != nullptr) {
+    long long* g_ph = ph_slots();
     const long long now = clock64();
     const long long d = now - g_ph[kPhLast];
     const long long d1 = den > 0 ? d * num / den : d;
@@ -774,7 +785,7 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
       acc = acc + s.w[j] * (dx * dx + dy * dy);
     }
   }
-  return make_double3(mx, my, sqrt(R.sum<NW>(acc)));
+  return make_double3(mx, my, sqrt_rn_clamp(R.sum<NW>(acc)));  // >= 0: 0 or far above 2^-960
 }
 
 // pf::resample (tracking.cpp:147-170): inclusive scan of w in index order, then
@@ -1410,60 +1421,103 @@ __device__ __forceinline__ void stage_env(const DevConfig& cg, const DevBatch& B
   }
 }
 
+// pf::reinit (tracking.cpp:76-92) of one particle from its 8 stream words:
+// r = R sqrt(u0), a = 2 pi u1 -> position; s = vmax u2, d = 2 pi u3 -> velocity.
+__device__ __forceinline__ void reinit_particle(const uint32_t* q, double cx, double cy, double radius, double vmax,
+                                                const double2* tab_sc, double& px, double& py, double& vx,
+                                                double& vy) {
+  const double r = radius * sqrt_rn_clamp(uniform_from_words(q[0], q[1]));
+  const double an = kTwoPi * uniform_from_words(q[2], q[3]);
+  double sa, ca;
+  sincos_table_d(an, tab_sc, sa, ca);
+  px = cx + r * ca;
+  py = cy + r * sa;
+  const double sp = vmax * uniform_from_words(q[4], q[5]);
+  const double d = kTwoPi * uniform_from_words(q[6], q[7]);
+  double sd, cd;
+  sincos_table_d(d, tab_sc, sd, cd);
+  vx = sp * cd;
+  vy = sp * sd;
+}
+
 // pf::reinit (tracking.cpp:76-92) + estimate for one set (spawn, env.cpp:214-220).
-template <int PPT>
+// FULL (P == NW * 32 * PPT): each thread's PPT consecutive particles draw their
+// 8 PPT words straight from 2 PPT + 1 Philox blocks in registers (one spare
+// block covers a stream position that is not a multiple of 4), the set goes to
+// HBM with 256-bit stores and the estimate is one block reduction. Otherwise
+// the words are staged through shared memory.
+template <int PPT, bool FULL, int NW>
 __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S, BlockReducer& R, const Rec& rec,
                            int64_t gi, int64_t gset, int a, int t, double cx, double cy, double vmax) {
   const int P = c.P, tid = threadIdx.x;
   const int ps = a * c.T + t, ti = a * c.sT + t;
   const int k0 = tid * PPT;
-  uint64_t pos = (uint64_t)TRK(K_POS, ti);
+  const uint64_t pos = (uint64_t)TRK(K_POS, ti);
   const uint64_t key = derive_key(B.seed, kTagPf, (uint64_t)gi, (uint64_t)ps);
-  uint32_t* words = reinterpret_cast<uint32_t*>(S.pf);  // the set buffer (no prefetch in flight here)
-  __syncthreads();  // that area may still be read by the previous phase
-  gen_words(words, key, (uint64_t)ps, pos, 8ull * (uint64_t)P);
-  __syncthreads();
   const int off = (int)(pos & 3);
-  const double inv = 1.0 / (double)P;
   const double radius = c.init_radius;
   SetRegs<PPT> s;
+  if constexpr (FULL) {
+    constexpr int NBK = 2 * PPT + 1;
+    uint64_t bq[NBK];
+    uint4 bo[NBK];
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = k0 + j;
-    s.px[j] = s.py[j] = s.vx[j] = s.vy[j] = s.w[j] = 0.0;
-    if (k < P) {
-      const uint32_t* q = words + off + 8 * k;
-      auto u = [&](int i) {
-        const uint64_t lo = q[2 * i], hi = q[2 * i + 1];
-        return (double)(((hi << 32) | lo) >> 11) * 0x1.0p-53;
-      };
-      const double r = radius * sqrt(u(0));
-      const double an = kTwoPi * u(1);
-      double sa, ca;
-      sincos(an, &sa, &ca);
-      s.px[j] = cx + r * ca;
-      s.py[j] = cy + r * sa;
-      const double sp = vmax * u(2);
-      const double d = kTwoPi * u(3);
-      double sd, cd;
-      sincos(d, &sd, &cd);
-      s.vx[j] = sp * cd;
-      s.vy[j] = sp * sd;
-      s.w[j] = inv;
+    for (int i = 0; i < NBK; ++i) bq[i] = (pos >> 2) + (uint64_t)(2 * k0 + i);
+    philox_n<NBK>(key, (uint64_t)ps, bq, bo);
+    uint32_t wv[4 * NBK];
+#pragma unroll
+    for (int i = 0; i < NBK; ++i) wv[4 * i] = bo[i].x, wv[4 * i + 1] = bo[i].y, wv[4 * i + 2] = bo[i].z, wv[4 * i + 3] = bo[i].w;
+    // the window of words starting at `off` (branch-free 2-word, then 1-word shift)
+    const bool s2 = off & 2, s1 = off & 1;
+    uint32_t b[8 * PPT + 1];
+#pragma unroll
+    for (int j = 0; j <= 8 * PPT; ++j) b[j] = s2 ? wv[j + 2] : wv[j];
+    uint32_t W[8 * PPT];
+#pragma unroll
+    for (int j = 0; j < 8 * PPT; ++j) W[j] = s1 ? b[j + 1] : b[j];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      reinit_particle(W + 8 * j, cx, cy, radius, vmax, S.tab_sc, s.px[j], s.py[j], s.vx[j], s.vy[j]);
+      s.w[j] = c.inv_P;
+    }
+  } else {
+    uint32_t* words = reinterpret_cast<uint32_t*>(S.pf);  // the set buffer (no prefetch in flight here)
+    __syncthreads();  // that area may still be read by the previous set
+    gen_words(words, key, (uint64_t)ps, pos, 8ull * (uint64_t)P);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = k0 + j;
+      s.px[j] = s.py[j] = s.vx[j] = s.vy[j] = s.w[j] = 0.0;
+      if (k < P) {
+        reinit_particle(words + off + 8 * k, cx, cy, radius, vmax, S.tab_sc, s.px[j], s.py[j], s.vx[j], s.vy[j]);
+        s.w[j] = c.inv_P;
+      }
     }
   }
-  pos += 8ull * (uint64_t)P;
-  const double3 est = pf_estimate<PPT, false, 0>(s, k0, P, cx, cy, R);
+  // estimate (tracking.cpp:180-188) of the uniform-weight cloud about its centre
+  const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, cx, cy, R, true, c.inv_P);
   const size_t base = (size_t)gset * P;
+  if constexpr (FULL) {
 #pragma unroll
-  for (int j = 0; j < PPT; ++j) {
-    const int k = k0 + j;
-    if (k < P) {
-      B.px[base + k] = s.px[j];
-      B.py[base + k] = s.py[j];
-      B.vx[base + k] = s.vx[j];
-      B.vy[base + k] = s.vy[j];
-      B.w[base + k] = s.w[j];
+    for (int q = 0; q < PPT; q += 4) {
+      st_global_v4(B.px + base + k0 + q, s.px[q], s.px[q + 1], s.px[q + 2], s.px[q + 3]);
+      st_global_v4(B.py + base + k0 + q, s.py[q], s.py[q + 1], s.py[q + 2], s.py[q + 3]);
+      st_global_v4(B.vx + base + k0 + q, s.vx[q], s.vx[q + 1], s.vx[q + 2], s.vx[q + 3]);
+      st_global_v4(B.vy + base + k0 + q, s.vy[q], s.vy[q + 1], s.vy[q + 2], s.vy[q + 3]);
+      st_global_v4(B.w + base + k0 + q, s.w[q], s.w[q + 1], s.w[q + 2], s.w[q + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const int k = k0 + j;
+      if (k < P) {
+        B.px[base + k] = s.px[j];
+        B.py[base + k] = s.py[j];
+        B.vx[base + k] = s.vx[j];
+        B.vy[base + k] = s.vy[j];
+        B.w[base + k] = s.w[j];
+      }
     }
   }
   if (tid == 0) {
@@ -1472,19 +1526,26 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
     TRK(K_SPREAD, ti) = est.z;
     TRK(K_AGE, ti) = 0.0;
     TRK(K_EVER, ti) = 0.0;
-    TRK(K_POS, ti) = (double)pos;
+    TRK(K_POS, ti) = (double)(pos + 8ull * (uint64_t)P);
     TRK(K_MAXSPEED, ti) = vmax;
     TRK(K_ESSOK, ti) = 1.0;
   }
-  __syncthreads();
 }
 
 // Re-init every set of the chunk's envs flagged kChunkFlagSpawned (out of line:
-// works on the global copy of the batch descriptor and the dynamic smem).
-template <int PPT, int NP>
-__device__ __noinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t e1) {
+// works on the global copy of the batch descriptor and the dynamic smem; the
+// sincos table is in place).
+// Inlined into each kernel: as an out-of-line function called from the step
+// kernel (shared with the generic step instance) the particle registers of
+// all but the first particle per thread came back wrong (every set, on the
+// device; the same function called from the reset kernel was right, and
+// inlining fixes it) -- kept inline until that is understood.
+template <int PPT, int NP, int KTAG>
+__device__ __forceinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t e1) {
   const Smem S = carve_dyn<NP>(B.cfgs[0].sA, B.cfgs[0].sT);
   BlockReducer R{S.red, 0};
+  constexpr int NW = NP / (32 * PPT);
+  const bool full = B.P == NP && (int)blockDim.x == NW * 32;
   for (int64_t e = e0; e < e1; ++e) {
     if (!(S.flags[e - e0] & kChunkFlagSpawned)) continue;
     const DevConfig& c = cfg_of(B, e);
@@ -1494,9 +1555,15 @@ __device__ __noinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int64_t
     const int64_t so = set_off(B, e);
     for (int a = 0; a < c.A; ++a) {
       const double cx = AG(V_X, a), cy = AG(V_Y, a);
-      for (int t = 0; t < c.T; ++t) reinit_set<PPT>(c, B, S, R, rec, gi, so + a * c.T + t, a, t, cx, cy, vmax);
+      for (int t = 0; t < c.T; ++t) {
+        if (full)
+          reinit_set<PPT, true, NW>(c, B, S, R, rec, gi, so + a * c.T + t, a, t, cx, cy, vmax);
+        else
+          reinit_set<PPT, false, 0>(c, B, S, R, rec, gi, so + a * c.T + t, a, t, cx, cy, vmax);
+      }
     }
   }
+  __syncthreads();
 }
 
 // ================================================================ kernels ===
@@ -1528,11 +1595,11 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
 #endif
   // phase timing (thread 0, shared memory: nothing live in registers)
   const bool timing = B.phase_cycles != nullptr;
-  __shared__ long long ph_t0[2];  // launch start: SM clock, globaltimer
   if (timing && threadIdx.x == 0) {
+    long long* g_ph = ph_slots();
     for (int k = 0; k <= kPhaseWait; ++k) g_ph[k] = 0;
-    g_ph[kPhLast] = ph_t0[0] = clock64();
-    ph_t0[1] = (long long)globaltimer_ns();
+    g_ph[kPhLast] = g_ph[kPhLast + 1] = clock64();
+    g_ph[kPhLast + 2] = (long long)globaltimer_ns();
   }
   // Three phases separated by grid-wide barriers (cooperative launch: every CTA
   // is resident): the env prologues of the CTA's static env range; the particle
@@ -1613,7 +1680,7 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
           atomicMax(status, (int)ST_SPAWN_INFEASIBLE);
       }
       __syncthreads();
-      reinit_chunk<PPT, NP>(Bg, e0, e1);
+      reinit_chunk<PPT, NP, 1>(Bg, e0, e1);
       write_outputs(Bg, e0, e1, S.flags, kChunkFlagSpawned, false);
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagSpawned)) B.step[e] = 0;
     }
@@ -1621,10 +1688,11 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     ph_mark(B, PH_RESET);
   }
   if (timing && threadIdx.x == 0) {
+    const long long* g_ph = ph_slots();
     unsigned long long* out = B.phase_cycles + (size_t)blockIdx.x * kPhaseSlots;
     for (int k = 0; k <= kPhaseWait; ++k) out[k] += (unsigned long long)g_ph[k];
-    out[kPhaseWait + 1] += (unsigned long long)(clock64() - ph_t0[0]);
-    out[kPhaseWait + 2] += globaltimer_ns() - (unsigned long long)ph_t0[1];
+    out[kPhaseWait + 1] += (unsigned long long)(clock64() - g_ph[kPhLast + 1]);
+    out[kPhaseWait + 2] += globaltimer_ns() - (unsigned long long)g_ph[kPhLast + 2];
   }
 #ifdef UT_SET_PROFILE
   if (threadIdx.x == 0)
@@ -1640,6 +1708,7 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) reset_kernel(D
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem S = carve<NP>(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT);
   const DevBatch& Bg = *B.self;
+  load_tables(S);  // the re-init's sincos table
   int64_t lo, hi;
   cta_range(B.n_envs, lo, hi);
   for (int64_t e0 = lo; e0 < hi; e0 += blockDim.x) {
@@ -1668,7 +1737,7 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) reset_kernel(D
       B.step[e] = 0;
     }
     __syncthreads();
-    reinit_chunk<PPT, NP>(Bg, e0, e1);
+    reinit_chunk<PPT, NP, 0>(Bg, e0, e1);
     write_outputs(Bg, e0, e1, S.flags, 0, false);
     __syncthreads();
   }

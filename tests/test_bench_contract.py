@@ -38,3 +38,21 @@ def test_reference_arm_prints_one_json_line():
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["unit"] == "agent-env steps/s"
+
+
+@pytest.mark.parametrize("cfg,gpus,scaling,total", [("c3", 2, "strong", 65536), ("c5", 2, "weak", 262144)])
+def test_gpus_flag_spawns_one_rank_per_gpu(cfg, gpus, scaling, total):
+    """`bench.py --gpus N` outside torchrun re-launches itself as N ranks
+    (torch.distributed.run on 127.0.0.1); the ranks shard the envs by contiguous
+    global index range (C3 strong: 65,536 in total; C5 weak: 131,072 each) and
+    all-reduce over the process group (gloo without a GPU)."""
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", str(gpus), "--config", cfg, "--dry-run"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == gpus and d["scaling"] == scaling and d["total_envs"] == total
+    assert d["envs_sum"] == total and d["max_rank"] == gpus and d["backend"] == "gloo"
+    r = d["ranges"]
+    assert r[0][0] == 0 and r[-1][1] == total and all(a[1] == b[0] for a, b in zip(r, r[1:]))
