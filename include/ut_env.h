@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define UT_ABI_VERSION 3
+#define UT_ABI_VERSION 4
 
 enum ut_status {
   UT_OK = 0,
@@ -243,6 +243,54 @@ int ut_vecenv_phase_ns(ut_vecenv* v, uint64_t out[UT_N_PHASES], int reset);
  * (env.cpp:234-504): a finished env keeps its terminal state and stays done
  * until reset; final_obs is not written. */
 int ut_vecenv_set_auto_reset(ut_vecenv* v, int on);
+
+/* ---- multi-device VecEnv ------------------------------------------------ */
+/* One VecEnv over several GPUs of one box, like the reference's one VecEnv over
+ * its worker threads (vecenv.hpp:26-27, sharded by env index at vecenv.cpp:83).
+ * Envs shard by contiguous global index range (shard i = envs
+ * [n_envs*i/n, n_envs*(i+1)/n)), each shard an ordinary ut_vecenv on
+ * device_ids[i] keyed by its global env indices, so the batch is bit-identical to
+ * a single-device VecEnv of the same n_envs and seed. Steps run on every device
+ * concurrently with no data-path collective; the statistics vector is
+ * all-reduced over NCCL (north_star). Homogeneous configs only. */
+typedef struct ut_multienv ut_multienv;
+enum {
+  UT_MULTI_STATS_AUTO = 0, /* NCCL when the device ids are distinct and n_devices > 1, else host */
+  UT_MULTI_STATS_NCCL = 1, /* always NCCL (also for one device); device ids must be distinct */
+  UT_MULTI_STATS_HOST = 2  /* the shards' vectors summed on the host, in shard order */
+};
+int ut_multienv_create(const ut_env_config* cfg, int64_t n_envs, uint64_t master_seed, const int32_t* device_ids,
+                       int32_t n_devices, int32_t stats_flags, ut_multienv** out);
+void ut_multienv_destroy(ut_multienv* m);
+int ut_multienv_n_shards(const ut_multienv* m);
+/* UT_MULTI_STATS_NCCL or UT_MULTI_STATS_HOST: how ut_multienv_stats reduces. */
+int ut_multienv_stats_backend(const ut_multienv* m);
+/* Shard i's single-device handle (for its device buffers), its global env range and device. */
+int ut_multienv_shard(ut_multienv* m, int32_t i, ut_vecenv** shard, int64_t* env_begin, int64_t* env_end,
+                      int32_t* device);
+/* The shard holding global env `env`, and its index inside that shard. */
+int ut_multienv_locate(ut_multienv* m, int64_t env, ut_vecenv** shard, int64_t* local_env);
+int ut_multienv_reset_all(ut_multienv* m);
+/* VecEnv::step with host actions, n_envs x n_agents row-major over the WHOLE batch;
+ * validated on every device before any env moves (lowest failing GLOBAL env). */
+int ut_multienv_step(ut_multienv* m, const int32_t* actions);
+int ut_multienv_step_policy(ut_multienv* m, int policy, int n_steps);
+int ut_multienv_refresh_outputs(ut_multienv* m);
+int ut_multienv_set_auto_reset(ut_multienv* m, int on);
+int ut_multienv_synchronize(ut_multienv* m);
+/* The whole batch's outputs in the single-handle layout (ut_buffers). */
+int ut_multienv_copy_outputs(ut_multienv* m, const ut_host_outputs* dst);
+/* Batch statistics, all-reduced over the shards (see UT_MULTI_STATS_*). */
+int ut_multienv_stats(ut_multienv* m, double out[UT_N_STATS], int reset);
+int ut_multienv_enable_phase_timing(ut_multienv* m, int on);
+int ut_multienv_phase_ns(ut_multienv* m, uint64_t out[UT_N_PHASES], int reset);
+int64_t ut_multienv_launch_count(const ut_multienv* m);
+/* env(i).serialize_state / deserialize_state / world().step by GLOBAL env index. */
+int ut_multienv_serialize(ut_multienv* m, int64_t env, double* blob, size_t cap, size_t* len);
+int ut_multienv_deserialize(ut_multienv* m, int64_t env, const double* blob, size_t len);
+int ut_multienv_world_step(ut_multienv* m, int64_t env, int32_t* step);
+/* ncclGetVersion of the NCCL the statistics all-reduce loads (UT_ERR_RUNTIME if none). */
+int ut_nccl_version(int* version);
 
 /* ---- per-env state (Environment API) ----------------------------------- */
 /* Environment::serialize_state / deserialize_state (env.cpp:550-659), identical

@@ -23,7 +23,7 @@ STAT_NAMES = (
     "eval_dist_sum", "eval_dist_sq", "eval_err_sum", "eval_err_sq", "eval_collided_episodes",
     "eval_lost_episodes",
 )
-UT_ABI_VERSION = 3
+UT_ABI_VERSION = 4
 UT_N_STATS = len(STAT_NAMES)
 
 

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "ut_env.h"
@@ -198,7 +199,17 @@ struct ut_vecenv {
   }
 
   int check_status(const char* what) {
+    int rc;
+    if ((rc = enqueue_status())) return rc;
+    return finish_status(what);
+  }
+  // The two halves of check_status, so a multi-device handle can have every
+  // device's work in flight before it waits on any of them.
+  int enqueue_status() {
     UT_CUDA(cudaMemcpyAsync(h_status, d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    return UT_OK;
+  }
+  int finish_status(const char* what) {
     UT_CUDA(cudaStreamSynchronize(stream));
     UT_CUDA(cudaGetLastError());
     if (h_status[0] == ST_SPAWN_INFEASIBLE) {
@@ -589,8 +600,11 @@ int ut_vecenv_reset_all(ut_vecenv* v) {
   return v->check_status("reset_all");
 }
 
-int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device) {
-  DeviceGuard dg(v->device);
+namespace {
+// First half of VecEnv::step (vecenv.cpp:79-93): stage the actions and validate
+// every env's actions on the device; nothing is mutated. The result is read by
+// validate_result() once the stream has reached it.
+int enqueue_validate(ut_vecenv* v, const int32_t* actions, int actions_on_device) {
   const size_t n = (size_t)(v->n_envs * v->A_max);
   UT_CUDA(cudaMemcpyAsync(const_cast<int32_t*>(v->B.actions), actions, n * sizeof(int32_t),
                           actions_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, v->stream));
@@ -600,24 +614,37 @@ int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device) 
   validate_kernel<<<(unsigned)((v->n_envs + tpb - 1) / tpb), tpb, 0, v->stream>>>(v->B);
   ++v->launches;
   UT_CUDA(cudaGetLastError());
-  UT_CUDA(cudaMemcpyAsync(v->h_status, v->d_status, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, v->stream));
+  return v->enqueue_status();
+}
+
+// UT_ERR_CONTRACT for the lowest env whose action failed validation, its index
+// shown as `shown_base + e` (the global index for a shard of a multi-device
+// handle); message format of env.cpp:241-246 prefixed like vecenv.cpp:88-93.
+int validate_result(ut_vecenv* v, int64_t shown_base) {
   UT_CUDA(cudaStreamSynchronize(v->stream));
-  if (v->h_status[1] != INT_MAX) {
-    // message format of env.cpp:241-246 prefixed like vecenv.cpp:88-93
-    const int64_t e = v->h_status[1];
-    std::vector<int32_t> acts((size_t)v->A_max);
-    UT_CUDA(cudaMemcpy(acts.data(), v->B.actions + e * v->A_max, sizeof(int32_t) * v->A_max, cudaMemcpyDeviceToHost));
-    std::vector<double> rec;
-    if ((rc = v->get_rec(e, rec))) return rc;
-    const DevConfig& d = v->cfg(e);
-    for (int a = 0; a < d.A; ++a) {
-      const int act = acts[(size_t)a], r = (int)rec[(size_t)(d.o_agent + V_RUDDER * d.sA + a)];
-      if (act < 0 || act >= UT_NUM_ACTIONS || std::abs(act - r) > 1)
-        return fail(UT_ERR_CONTRACT, "env %lld: step: invalid action %d for agent %d at rudder index %d", (long long)e,
-                    act, a, r);
-    }
-    return fail(UT_ERR_CONTRACT, "env %lld: step: invalid action", (long long)e);
+  if (v->h_status[1] == INT_MAX) return UT_OK;
+  const int64_t e = v->h_status[1];
+  const long long shown = (long long)(shown_base + e);
+  std::vector<int32_t> acts((size_t)v->A_max);
+  UT_CUDA(cudaMemcpy(acts.data(), v->B.actions + e * v->A_max, sizeof(int32_t) * v->A_max, cudaMemcpyDeviceToHost));
+  std::vector<double> rec;
+  int rc;
+  if ((rc = v->get_rec(e, rec))) return rc;
+  const DevConfig& d = v->cfg(e);
+  for (int a = 0; a < d.A; ++a) {
+    const int act = acts[(size_t)a], r = (int)rec[(size_t)(d.o_agent + V_RUDDER * d.sA + a)];
+    if (act < 0 || act >= UT_NUM_ACTIONS || std::abs(act - r) > 1)
+      return fail(UT_ERR_CONTRACT, "env %lld: step: invalid action %d for agent %d at rudder index %d", shown, act, a,
+                  r);
   }
+  return fail(UT_ERR_CONTRACT, "env %lld: step: invalid action", shown);
+}
+}  // namespace
+
+int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device) {
+  DeviceGuard dg(v->device);
+  int rc;
+  if ((rc = enqueue_validate(v, actions, actions_on_device)) || (rc = validate_result(v, 0))) return rc;
   if ((rc = v->launch_step(MODE_EXTERNAL))) return rc;
   return v->check_status("step");
 }
@@ -1401,3 +1428,6 @@ int ut_debug_derive_key(uint64_t a, uint64_t b, uint64_t c, uint64_t dd, int dev
   return UT_OK;
 }
 }  // extern "C"
+
+// ------------------------------------------------- multi-device handle ---
+#include "ut_multi.cuh"
