@@ -26,6 +26,11 @@ struct ut_vecenv;
  * in the generic step instance: particle counts other than 256/512/1024 or
  * noise-free configs). */
 int ut_debug_set_knobs(struct ut_vecenv* v, int force_exact, int64_t trace_env);
+/* Grid-size invariance (the device analogue of the reference's worker-count
+ * invariance, test_vecenv.cpp:126-143): runs the step / reset kernels on `ctas`
+ * co-resident CTAs (1 .. the default grid; 0 restores the default), which
+ * changes every CTA's static env range and the dynamic set schedule. */
+int ut_debug_set_grid(struct ut_vecenv* v, int32_t ctas);
 /* Per-CTA busy cycles (every phase, not the grid-barrier waits) of the step
  * kernel since phase timing was enabled
  * (ut_vecenv_enable_phase_timing): *n = grid size; out may be NULL to query it.

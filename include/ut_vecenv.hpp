@@ -78,6 +78,43 @@ struct StepOutput {
   std::vector<uint8_t> target_lost;
 };
 
+namespace detail {
+// Host mirrors of the batch buffers (vecenv.hpp:51-62), filled by one
+// ut_host_outputs copy (single- or multi-device).
+struct HostMirror {
+  ColMajor obs, global, final_obs;
+  std::vector<double> rewards;
+  std::vector<uint8_t> dones, masks;
+  std::vector<StepOutput> infos;
+
+  template <class Copy>
+  void fill(int64_t E, int64_t A, int64_t T, int64_t R, Copy&& copy) {
+    obs = {std::vector<double>(E * A * R * UT_FEATURE_DIM), E * A * R, UT_FEATURE_DIM};
+    final_obs = {std::vector<double>(E * A * R * UT_FEATURE_DIM), E * A * R, UT_FEATURE_DIM};
+    global = {std::vector<double>(E * R * UT_FEATURE_DIM), E * R, UT_FEATURE_DIM};
+    rewards.assign(E, 0.0);
+    dones.assign(E, 0);
+    masks.assign(E * A * UT_NUM_ACTIONS, 0);
+    std::vector<double> err(E * T), dist(E * T);
+    std::vector<uint8_t> lost(E * T), coll(E);
+    ut_host_outputs o{obs.data.data(), final_obs.data.data(), global.data.data(), rewards.data(),
+                      dones.data(),    masks.data(),          err.data(),         dist.data(),
+                      lost.data(),     coll.data(),           nullptr};
+    check(copy(&o));
+    infos.resize(E);
+    for (int64_t e = 0; e < E; ++e) {
+      StepOutput& s = infos[e];
+      s.reward = rewards[e];
+      s.done = dones[e] != 0;
+      s.collision = coll[e] != 0;
+      s.tracking_error.assign(err.begin() + e * T, err.begin() + (e + 1) * T);
+      s.min_agent_dist.assign(dist.begin() + e * T, dist.begin() + (e + 1) * T);
+      s.target_lost.assign(lost.begin() + e * T, lost.begin() + (e + 1) * T);
+    }
+  }
+};
+}  // namespace detail
+
 class VecEnv {
  public:
   // VecEnv(cfg, n_envs, master_seed, workers) (vecenv.hpp:26-27); `workers` has
@@ -115,13 +152,13 @@ class VecEnv {
   void step_policy(BenchmarkPolicy p) { check(ut_vecenv_step_policy(h_, static_cast<int>(p), 1)), dirty_ = true; }
   void refresh_outputs() { check(ut_vecenv_refresh_outputs(h_)), dirty_ = true; }
 
-  const ColMajor& obs_stack() { return pull(), obs_; }
-  const ColMajor& global_stack() { return pull(), global_; }
-  const ColMajor& final_obs_stack() { return pull(), final_obs_; }
-  const std::vector<double>& rewards() { return pull(), rewards_; }
-  const std::vector<uint8_t>& dones() { return pull(), dones_; }
-  const std::vector<uint8_t>& masks() { return pull(), masks_; }
-  const std::vector<StepOutput>& infos() { return pull(), infos_; }
+  const ColMajor& obs_stack() { return pull(), m_.obs; }
+  const ColMajor& global_stack() { return pull(), m_.global; }
+  const ColMajor& final_obs_stack() { return pull(), m_.final_obs; }
+  const std::vector<double>& rewards() { return pull(), m_.rewards; }
+  const std::vector<uint8_t>& dones() { return pull(), m_.dones; }
+  const std::vector<uint8_t>& masks() { return pull(), m_.masks; }
+  const std::vector<StepOutput>& infos() { return pull(), m_.infos; }
 
   // env(i) surface used by the trainer: world().step, serialize/deserialize
   int32_t world_step(int64_t env) const {
@@ -160,28 +197,8 @@ class VecEnv {
  private:
   void pull() {
     if (!dirty_) return;
-    const int64_t E = n_envs_, A = buf_.n_agents, T = buf_.n_targets;
-    obs_ = {std::vector<double>(buf_.obs_rows * UT_FEATURE_DIM), buf_.obs_rows, UT_FEATURE_DIM};
-    final_obs_ = {std::vector<double>(buf_.obs_rows * UT_FEATURE_DIM), buf_.obs_rows, UT_FEATURE_DIM};
-    global_ = {std::vector<double>(buf_.global_rows * UT_FEATURE_DIM), buf_.global_rows, UT_FEATURE_DIM};
-    rewards_.assign(E, 0.0);
-    dones_.assign(E, 0);
-    masks_.assign(E * A * UT_NUM_ACTIONS, 0);
-    std::vector<double> err(E * T), dist(E * T);
-    std::vector<uint8_t> lost(E * T), coll(E);
-    ut_host_outputs o{obs_.data.data(), final_obs_.data.data(), global_.data.data(), rewards_.data(),
-                      dones_.data(), masks_.data(), err.data(), dist.data(), lost.data(), coll.data(), nullptr};
-    check(ut_vecenv_copy_outputs(h_, &o));
-    infos_.resize(E);
-    for (int64_t e = 0; e < E; ++e) {
-      StepOutput& s = infos_[e];
-      s.reward = rewards_[e];
-      s.done = dones_[e] != 0;
-      s.collision = coll[e] != 0;
-      s.tracking_error.assign(err.begin() + e * T, err.begin() + (e + 1) * T);
-      s.min_agent_dist.assign(dist.begin() + e * T, dist.begin() + (e + 1) * T);
-      s.target_lost.assign(lost.begin() + e * T, lost.begin() + (e + 1) * T);
-    }
+    m_.fill(n_envs_, buf_.n_agents, buf_.n_targets, buf_.n_rows,
+            [&](const ut_host_outputs* o) { return ut_vecenv_copy_outputs(h_, o); });
     dirty_ = false;
   }
 
@@ -189,10 +206,101 @@ class VecEnv {
   int n_envs_;
   ut_buffers buf_{};
   bool dirty_ = true;
-  ColMajor obs_, global_, final_obs_;
-  std::vector<double> rewards_;
-  std::vector<uint8_t> dones_, masks_;
-  std::vector<StepOutput> infos_;
+  detail::HostMirror m_;
+};
+
+
+// One VecEnv over several GPUs (ut_multienv_*): the reference's VecEnv surface
+// (vecenv.hpp:26-104) with the envs sharded by index range over `devices`
+// instead of worker threads; bit-identical to VecEnv(cfg, n_envs, seed) on one
+// device. stats() is the batch total, all-reduced over NCCL.
+class MultiVecEnv {
+ public:
+  MultiVecEnv(const EnvConfig& cfg, int n_envs, std::uint64_t master_seed, const std::vector<int>& devices,
+              int stats_flags = UT_MULTI_STATS_AUTO)
+      : n_envs_(n_envs), A_(cfg.n_agents), T_(cfg.n_targets) {
+    std::vector<int32_t> d(devices.begin(), devices.end());
+    check(ut_multienv_create(&cfg, n_envs, master_seed, d.data(), static_cast<int32_t>(d.size()), stats_flags, &h_));
+  }
+  ~MultiVecEnv() {
+    if (h_) ut_multienv_destroy(h_);
+  }
+  MultiVecEnv(const MultiVecEnv&) = delete;
+  MultiVecEnv& operator=(const MultiVecEnv&) = delete;
+
+  int n_envs() const { return n_envs_; }
+  int n_agents() const { return A_; }
+  int n_rows() const { return A_ + T_; }
+  int n_shards() const { return ut_multienv_n_shards(h_); }
+  bool nccl_stats() const { return ut_multienv_stats_backend(h_) == UT_MULTI_STATS_NCCL; }
+
+  void reset_all() { check(ut_multienv_reset_all(h_)), dirty_ = true; }
+  void step(const int* actions, size_t n) {
+    if (n != static_cast<size_t>(n_envs_) * static_cast<size_t>(A_))
+      throw ContractViolation("vecenv step: wrong action count");
+    check(ut_multienv_step(h_, reinterpret_cast<const int32_t*>(actions)));
+    dirty_ = true;
+  }
+  template <class Span>
+  void step(const Span& actions) {
+    step(actions.data(), actions.size());
+  }
+  void step_policy(BenchmarkPolicy p, int n_steps = 1) {
+    check(ut_multienv_step_policy(h_, static_cast<int>(p), n_steps)), dirty_ = true;
+  }
+  void refresh_outputs() { check(ut_multienv_refresh_outputs(h_)), dirty_ = true; }
+
+  const ColMajor& obs_stack() { return pull(), m_.obs; }
+  const ColMajor& global_stack() { return pull(), m_.global; }
+  const ColMajor& final_obs_stack() { return pull(), m_.final_obs; }
+  const std::vector<double>& rewards() { return pull(), m_.rewards; }
+  const std::vector<uint8_t>& dones() { return pull(), m_.dones; }
+  const std::vector<uint8_t>& masks() { return pull(), m_.masks; }
+  const std::vector<StepOutput>& infos() { return pull(), m_.infos; }
+
+  int32_t world_step(int64_t env) const {
+    int32_t s = 0;
+    check(ut_multienv_world_step(h_, env, &s));
+    return s;
+  }
+  std::vector<double> serialize_state(int64_t env) const {
+    size_t len = 0;
+    check(ut_multienv_serialize(h_, env, nullptr, 0, &len));
+    std::vector<double> blob(len);
+    check(ut_multienv_serialize(h_, env, blob.data(), blob.size(), &len));
+    return blob;
+  }
+  void deserialize_state(int64_t env, const std::vector<double>& blob) {
+    check(ut_multienv_deserialize(h_, env, blob.data(), blob.size()));
+    dirty_ = true;
+  }
+  // episode statistics (UT_STAT_*), the batch totals
+  std::vector<double> stats(bool reset = false) {
+    std::vector<double> s(UT_N_STATS);
+    check(ut_multienv_stats(h_, s.data(), reset ? 1 : 0));
+    return s;
+  }
+  // shard i's device buffers and its global env range
+  ut_buffers device_buffers(int shard, int64_t* env_begin = nullptr, int64_t* env_end = nullptr) const {
+    ut_vecenv* v = nullptr;
+    check(ut_multienv_shard(h_, shard, &v, env_begin, env_end, nullptr));
+    ut_buffers b{};
+    check(ut_vecenv_buffers(v, &b));
+    return b;
+  }
+  ut_multienv* handle() const { return h_; }
+
+ private:
+  void pull() {
+    if (!dirty_) return;
+    m_.fill(n_envs_, A_, T_, A_ + T_, [&](const ut_host_outputs* o) { return ut_multienv_copy_outputs(h_, o); });
+    dirty_ = false;
+  }
+
+  ut_multienv* h_ = nullptr;
+  int n_envs_, A_, T_;
+  bool dirty_ = true;
+  detail::HostMirror m_;
 };
 
 // benchmark_sps (vecenv.hpp:102-104), device-timed

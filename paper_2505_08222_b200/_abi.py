@@ -13,6 +13,7 @@ UT_REWARD_TRACKING, UT_REWARD_FOLLOW = 0, 1
 UT_POLICY_RANDOM, UT_POLICY_SCRIPTED = 0, 1
 UT_HEADING_DEFAULT, UT_HEADING_BUCKET = 0, 1
 UT_STREAM_LEGACY = 1  # cudaStreamLegacy
+UT_MULTI_STATS_AUTO, UT_MULTI_STATS_NCCL, UT_MULTI_STATS_HOST = 0, 1, 2
 # UT_PHASE_* (ut_env.h): the reference's seven StepPhase values, then the auto-reset
 PHASE_NAMES = ("targets", "agents", "measure", "filter", "comms", "observe", "reward", "reset")
 UT_N_PHASES = len(PHASE_NAMES)
@@ -135,6 +136,27 @@ def declare_product(lib):
                                        C.POINTER(BenchmarkReport)]),
         "ut_vecenv_enable_phase_timing": (C.c_int, [P, C.c_int]),
         "ut_vecenv_phase_cycles": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int]),
+        "ut_multienv_create": (C.c_int, [cfgp, I64, U64, C.POINTER(I32), I32, I32, C.POINTER(P)]),
+        "ut_multienv_destroy": (None, [P]),
+        "ut_multienv_n_shards": (C.c_int, [P]),
+        "ut_multienv_stats_backend": (C.c_int, [P]),
+        "ut_multienv_shard": (C.c_int, [P, I32, C.POINTER(P), C.POINTER(I64), C.POINTER(I64), C.POINTER(I32)]),
+        "ut_multienv_locate": (C.c_int, [P, I64, C.POINTER(P), C.POINTER(I64)]),
+        "ut_multienv_reset_all": (C.c_int, [P]),
+        "ut_multienv_step": (C.c_int, [P, P]),
+        "ut_multienv_step_policy": (C.c_int, [P, C.c_int, C.c_int]),
+        "ut_multienv_refresh_outputs": (C.c_int, [P]),
+        "ut_multienv_set_auto_reset": (C.c_int, [P, C.c_int]),
+        "ut_multienv_synchronize": (C.c_int, [P]),
+        "ut_multienv_copy_outputs": (C.c_int, [P, C.POINTER(HostOutputs)]),
+        "ut_multienv_stats": (C.c_int, [P, C.POINTER(C.c_double), C.c_int]),
+        "ut_multienv_enable_phase_timing": (C.c_int, [P, C.c_int]),
+        "ut_multienv_phase_ns": (C.c_int, [P, C.POINTER(C.c_uint64), C.c_int]),
+        "ut_multienv_launch_count": (I64, [P]),
+        "ut_multienv_serialize": (C.c_int, [P, I64, C.POINTER(C.c_double), C.c_size_t, C.POINTER(C.c_size_t)]),
+        "ut_multienv_deserialize": (C.c_int, [P, I64, C.POINTER(C.c_double), C.c_size_t]),
+        "ut_multienv_world_step": (C.c_int, [P, I64, C.POINTER(I32)]),
+        "ut_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
         "ut_last_error": (C.c_char_p, []),
         "ut_abi_version": (C.c_int, []),
     }
@@ -163,6 +185,8 @@ def declare_debug(lib):
     lib.ut_debug_ieee_check.restype = C.c_int
     lib.ut_debug_set_knobs.argtypes = [C.c_void_p, C.c_int, C.c_int64]
     lib.ut_debug_set_knobs.restype = C.c_int
+    lib.ut_debug_set_grid.argtypes = [C.c_void_p, C.c_int32]
+    lib.ut_debug_set_grid.restype = C.c_int
     lib.ut_debug_instance.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     lib.ut_debug_instance.restype = C.c_int
     return lib
@@ -178,5 +202,11 @@ PRODUCT_SYMBOLS = (
     "ut_vecenv_copy_outputs_async", "ut_vecenv_capture_trajectory", "ut_vecenv_trajectory_rows",
     "ut_vecenv_enable_phase_timing", "ut_vecenv_phase_cycles", "ut_vecenv_phase_ns",
     "ut_vecenv_wait_stream", "ut_vecenv_set_auto_reset",
+    "ut_multienv_create", "ut_multienv_destroy", "ut_multienv_n_shards", "ut_multienv_stats_backend",
+    "ut_multienv_shard", "ut_multienv_locate", "ut_multienv_reset_all", "ut_multienv_step",
+    "ut_multienv_step_policy", "ut_multienv_refresh_outputs", "ut_multienv_set_auto_reset",
+    "ut_multienv_synchronize", "ut_multienv_copy_outputs", "ut_multienv_stats",
+    "ut_multienv_enable_phase_timing", "ut_multienv_phase_ns", "ut_multienv_launch_count",
+    "ut_multienv_serialize", "ut_multienv_deserialize", "ut_multienv_world_step", "ut_nccl_version",
     "ut_last_error", "ut_abi_version",
 )

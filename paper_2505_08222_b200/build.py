@@ -15,6 +15,10 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libutrack_b200.so"
+# Test-only builds of the same sources (tests/test_gpu_race_shake.py): the race
+# shaker (ut_device.cuh, UT_RACE_SHAKE). Never loaded by the product path.
+VARIANTS = {"ut_race_shake": ["-DUT_RACE_SHAKE=0x5eed"]}
+VARIANT_DIR = LIB_DIR / "variants"
 SOURCES = [CSRC / "ut_capi.cu"]
 DEPS = SOURCES + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "ut_env.h"]
 
@@ -35,27 +39,42 @@ def nvcc():
     raise RuntimeError("nvcc not found")
 
 
-def up_to_date():
-    if not LIB.exists():
+def up_to_date(path):
+    if not path.exists():
         return False
-    t = LIB.stat().st_mtime
+    t = path.stat().st_mtime
     return all(p.stat().st_mtime <= t for p in DEPS)
 
 
+def variant_path(name):
+    return VARIANT_DIR / f"{name}.so"
+
+
 def build_native(force=False, verbose=False):
-    if not force and up_to_date():
-        return LIB
+    """The product library and the test variants, compiled concurrently."""
     LIB_DIR.mkdir(exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *map(str, SOURCES)]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed for libutrack_b200.so")
-    (LIB_DIR / "ptxas.log").write_text(res.stdout + res.stderr)
-    if verbose:
-        sys.stdout.write(res.stderr)
-    os.replace(tmp, LIB)
+    VARIANT_DIR.mkdir(exist_ok=True)
+    jobs = []
+    if force or not up_to_date(LIB):
+        jobs.append((LIB, []))
+    for name, defines in VARIANTS.items():
+        if force or not up_to_date(variant_path(name)):
+            jobs.append((variant_path(name), defines))
+    procs = []
+    for out, defines in jobs:
+        tmp = out.with_suffix(".so.tmp")
+        cmd = [nvcc(), *NVCC_FLAGS, *defines, "-o", str(tmp), *map(str, SOURCES)]
+        procs.append((out, tmp, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    for out, tmp, proc in procs:
+        so, se = proc.communicate()
+        if proc.returncode != 0:
+            sys.stderr.write(so + se)
+            raise RuntimeError(f"nvcc failed for {out.name}")
+        if out == LIB:
+            (LIB_DIR / "ptxas.log").write_text(so + se)
+            if verbose:
+                sys.stdout.write(se)
+        os.replace(tmp, out)
     return LIB
 
 

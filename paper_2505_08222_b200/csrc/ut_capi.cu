@@ -151,7 +151,7 @@ struct ut_vecenv {
   std::vector<int64_t> set_off;
   int64_t total_sets = 0;
   int A_max = 0, T_max = 0, R_max = 0, P = 0, rec_words = 0;
-  int nt = 0, grid = 0;
+  int nt = 0, grid = 0, grid_max = 0;
   size_t smem = 0;
   DevBatch B{};
   std::vector<void*> allocs;
@@ -476,6 +476,7 @@ int build(ut_vecenv* v, const ut_env_config* cfgs, int n_cfg, const int32_t* cfg
   // debug knob (occupancy experiments): cap resident CTAs per SM
   if (const char* cap = getenv("UT_DEBUG_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(cap)));
   v->grid = (int)std::min<int64_t>(n_envs, (int64_t)per_sm * sms);
+  v->grid_max = v->grid;
   if ((rc = v->alloc(&B.work, 1))) return rc;
   UT_CUDA(cudaMemsetAsync(B.work, 0, sizeof(int), v->stream));
   if ((rc = v->alloc(&v->d_self, 1))) return rc;
@@ -879,8 +880,8 @@ int ut_vecenv_enable_phase_timing(ut_vecenv* v, int on) {
   UT_CUDA(cudaStreamSynchronize(v->stream));
   if (on && !v->phase_buf) {
     int rc;
-    if ((rc = v->alloc(&v->phase_buf, (size_t)v->grid * kPhaseSlots))) return rc;
-    UT_CUDA(cudaMemset(v->phase_buf, 0, sizeof(unsigned long long) * v->grid * kPhaseSlots));
+    if ((rc = v->alloc(&v->phase_buf, (size_t)v->grid_max * kPhaseSlots))) return rc;
+    UT_CUDA(cudaMemset(v->phase_buf, 0, sizeof(unsigned long long) * v->grid_max * kPhaseSlots));
   }
   v->B.phase_cycles = on ? v->phase_buf : nullptr;
   return v->sync_batch();
@@ -896,10 +897,10 @@ int phase_sums(ut_vecenv* v, uint64_t cyc[UT_N_PHASES], double* ns_per_cycle, in
   *ns_per_cycle = 0.0;
   if (!v->phase_buf) return UT_OK;
   UT_CUDA(cudaStreamSynchronize(v->stream));
-  std::vector<unsigned long long> h((size_t)v->grid * kPhaseSlots);
+  std::vector<unsigned long long> h((size_t)v->grid_max * kPhaseSlots);
   UT_CUDA(cudaMemcpy(h.data(), v->phase_buf, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
   double c = 0.0, t = 0.0;
-  for (int b = 0; b < v->grid; ++b) {
+  for (int b = 0; b < v->grid_max; ++b) {
     const unsigned long long* r = h.data() + (size_t)b * kPhaseSlots;
     for (int k = 0; k < kPhaseCount; ++k) cyc[k] += r[k];
     c += (double)r[kPhaseWait + 1];
@@ -1306,6 +1307,14 @@ int ut_debug_set_knobs(ut_vecenv* v, int force_exact, int64_t trace_env) {
   v->B.force_exact = force_exact;
   v->B.trace_env = trace_env;
   return v->sync_batch();
+}
+int ut_debug_set_grid(ut_vecenv* v, int32_t ctas) {
+  DeviceGuard dg(v->device);
+  if (ctas < 0 || ctas > v->grid_max)
+    return fail(UT_ERR_CONTRACT, "set_grid: %d CTAs outside [1, %d] (0 = the default)", ctas, v->grid_max);
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  v->grid = ctas ? ctas : v->grid_max;
+  return UT_OK;
 }
 int ut_debug_instance(ut_vecenv* v, int32_t* full, int32_t* np) {
   DeviceGuard dg(v->device);

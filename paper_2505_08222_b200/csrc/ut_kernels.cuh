@@ -830,7 +830,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
 #pragma unroll
     for (int i = 0; i < PPT; i += 4) *reinterpret_cast<int4*>(mark + k0 + i) = make_int4(0, 0, 0, 0);
   }
-  __syncthreads();
+  ut_bar();
   double woff = 0.0;  // cum[k] = (sum of earlier warps' totals + excl) + loc[q]
   if constexpr (NW > 0) {
 #pragma unroll
@@ -868,7 +868,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
     const int hn = q + 1 < PPT ? hq[q + 1] : nxt;
     red_max_shared_if(hq[q] < P && hq[q] != hn, mark + min(hq[q], P - 1), k0 + q + 1);
   }
-  __syncthreads();
+  ut_bar();
   int r[PPT];
 #pragma unroll
   for (int i = 0; i < PPT; i += 4) {
@@ -892,7 +892,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
   if (!below) mex = -1;
   int* wmx = reinterpret_cast<int*>(wsum + 96);
   st_shared_if(lane == 31, reinterpret_cast<uint32_t*>(wmx) + warp, (uint32_t)wtop);
-  __syncthreads();
+  ut_bar();
   if constexpr (NW > 0) {
 #pragma unroll
     for (int v = 0; v < NW - 1; ++v)
@@ -948,6 +948,7 @@ __device__ unsigned long long g_setprof[kSetProfSlots];
 
 // Issue the TMA prefetch of particle set g (5 fields x P doubles) into S.pf.
 __device__ __forceinline__ void prefetch_set(const DevBatch& B, const Smem& S, int64_t g, int P) {
+  UT_SHAKE(5);
   const uint32_t bytes = (uint32_t)(sizeof(double) * P);
   const size_t off = (size_t)g * P;
   fence_proxy_async();
@@ -1115,6 +1116,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   if (FULL) {
     SETPROF(0);
     mbar_wait_sa(S.mbar_sa, tphase);
+    UT_SHAKE(6);
     SETPROF(1);
     tphase ^= 1u;
 #pragma unroll
@@ -1220,7 +1222,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     if (nm & 1) stage_max(nm - 1, stage(nm - 1));
     if (merged) load_field<PPT>(S.pf + 4 * NPf, k0, s.w);
     SETPROF(3);
-    __syncthreads();
+    ut_bar();
     double shift = 0.0;  // sum_j s'_j, in stage order
     const uint32_t* mbu = reinterpret_cast<const uint32_t*>(mb);
     for (int j = 0; j < nm; ++j) {
@@ -1281,7 +1283,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   }
   if (exact && nm > 0) {
     if (tid == 0) S.bc[kBcStatExact] += 1.0;
-    __syncthreads();  // every thread holds its particles: S.pf becomes the staging area
+    ut_bar();  // every thread holds its particles: S.pf becomes the staging area
 #pragma unroll
     for (int q = 0; q < PPT; ++q)
       if (FULL || k0 + q < P) {
@@ -1294,7 +1296,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
 #pragma unroll
     for (int q = 0; q < PPT; ++q)
       if (FULL || k0 + q < P) s.w[q] = S.cum[k0 + q];
-    __syncthreads();  // the staging area is reused by the resample
+    ut_bar();  // the staging area is reused by the resample
   }
   const bool fresh = nm > 0;
   // the update pass: the own ping's share is filter_step, the senders' comms
@@ -1482,9 +1484,9 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
     }
   } else {
     uint32_t* words = reinterpret_cast<uint32_t*>(S.pf);  // the set buffer (no prefetch in flight here)
-    __syncthreads();  // that area may still be read by the previous set
+    ut_bar();  // that area may still be read by the previous set
     gen_words(words, key, (uint64_t)ps, pos, 8ull * (uint64_t)P);
-    __syncthreads();
+    ut_bar();
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
       const int k = k0 + j;
@@ -1563,7 +1565,7 @@ __device__ __forceinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int6
       }
     }
   }
-  __syncthreads();
+  ut_bar();
 }
 
 // ================================================================ kernels ===
@@ -1587,7 +1589,7 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     cta_range(B.n_envs, lo64, hi64);
     lo = (int)lo64, hi = (int)hi64;
   }
-  __syncthreads();
+  ut_bar();
   uint32_t tphase = 0;
 #ifdef UT_SET_PROFILE
   if (threadIdx.x == 0)
@@ -1613,7 +1615,9 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     const int e = e0 + threadIdx.x;
     if (e < min(hi, e0 + (int)blockDim.x)) env_prologue(cfg_of(Bg, e), Bg, e, B.env_index_offset + e, mode);
   }
+  UT_SHAKE(1);
   grid.sync();  // every env's ping schedule is in place
+  UT_SHAKE(2);
   ph_mark(B, kPhaseWait);
   // ---- 2. particle sets, env by env from the work counter; the next env is
   // claimed at the start of the current one so its first set can be prefetched
@@ -1623,12 +1627,12 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     *claim = e;
     if (FULL && e < n) prefetch_set(B, S, set_off(B, e), B.P);
   }
-  __syncthreads();
+  ut_bar();
   int e = *claim;
   while (e < n) {
     stage_env(cfg_of(B, e), B, S, rec_of(B, e), e);
     if (threadIdx.x == 0) *claim = atomicAdd(B.work, 1);
-    __syncthreads();
+    ut_bar();
     const int en = *claim;
     const DevConfig& c = *S.cfg;
     const int so = (int)set_off(B, e);
@@ -1640,7 +1644,7 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
         const int last = a == nA - 1 && t == nT - 1;
         step_set<PPT, FULL, FULL ? NP / (32 * PPT) : 0>(c, B, S, R, e, g, a, t, tphase, last ? first_next : g + 1);
       }
-    __syncthreads();  // S.cfg / meas / mlist / claim reused by the next env
+    ut_bar();  // S.cfg / meas / mlist / claim reused by the next env
     if (threadIdx.x == 0) {  // the env's filter statistics, accumulated in smem per set
       const DevConfig& cg = cfg_of(B, e);
       double* st = B.rec + e + (int64_t)cg.o_stats * B.n_envs;
@@ -1651,7 +1655,9 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     e = en;
   }
   ph_mark(B, PH_FILTER);
+  UT_SHAKE(3);
   grid.sync();  // every estimate is in place
+  UT_SHAKE(4);
   ph_mark(B, kPhaseWait);
   if (blockIdx.x == 0 && threadIdx.x == 0) *B.work = 0;  // for the next launch
   for (int e0 = lo; e0 < hi; e0 += blockDim.x) {
@@ -1661,7 +1667,7 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
       const int e = e0 + threadIdx.x;
       if (e < e1) S.flags[threadIdx.x] = env_epilogue(cfg_of(Bg, e), Bg, e) ? kChunkFlagDone : 0;
     }
-    __syncthreads();
+    ut_bar();
     ph_mark(B, PH_REWARD);
     write_outputs(Bg, e0, e1, S.flags, 0, false);
     // terminal obs of finished envs (VecEnv auto-reset only)
@@ -1671,7 +1677,7 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     bool any = false;
     for (int i = 0; i < (int)(e1 - e0); ++i) any |= (S.flags[i] & kChunkFlagDone) != 0;
     if (any && B.auto_reset) {
-      __syncthreads();
+      ut_bar();
       const int e = e0 + threadIdx.x;
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagDone)) {
         if (spawn_serial(cfg_of(Bg, e), Bg, e, B.env_index_offset + e))
@@ -1679,12 +1685,12 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
         else
           atomicMax(status, (int)ST_SPAWN_INFEASIBLE);
       }
-      __syncthreads();
+      ut_bar();
       reinit_chunk<PPT, NP, 1>(Bg, e0, e1);
       write_outputs(Bg, e0, e1, S.flags, kChunkFlagSpawned, false);
       if (e < e1 && (S.flags[threadIdx.x] & kChunkFlagSpawned)) B.step[e] = 0;
     }
-    __syncthreads();
+    ut_bar();
     ph_mark(B, PH_RESET);
   }
   if (timing && threadIdx.x == 0) {
@@ -1736,10 +1742,10 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) reset_kernel(D
       B.dones[e] = 0;
       B.step[e] = 0;
     }
-    __syncthreads();
+    ut_bar();
     reinit_chunk<PPT, NP, 0>(Bg, e0, e1);
     write_outputs(Bg, e0, e1, S.flags, 0, false);
-    __syncthreads();
+    ut_bar();
   }
 }
 

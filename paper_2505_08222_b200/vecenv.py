@@ -487,6 +487,125 @@ class VecEnv:
             pass
 
 
+class MultiVecEnv:
+    """One VecEnv over several GPUs of one box (ut_multienv_*): the reference's
+    single VecEnv over all envs (vecenv.hpp:26-27), sharded by contiguous env index
+    range over ``devices`` instead of worker threads (vecenv.cpp:83). Bit-identical
+    to ``VecEnv(cfg, n_envs, seed)``; the statistics are all-reduced over NCCL
+    (``stats_backend() == "nccl"``), or summed on the host when a device repeats."""
+
+    _BACKENDS = {"auto": _abi.UT_MULTI_STATS_AUTO, "nccl": _abi.UT_MULTI_STATS_NCCL,
+                 "host": _abi.UT_MULTI_STATS_HOST}
+
+    def __init__(self, cfg: EnvConfig, n_envs: int, master_seed: int, devices: Sequence[int] = (0,),
+                 stats: str = "auto"):
+        self._lib = lib()
+        self._h = C.c_void_p()
+        c = cfg.to_c()
+        dev = (C.c_int32 * len(devices))(*devices)
+        _check(self._lib.ut_multienv_create(C.byref(c), n_envs, master_seed, dev, len(devices),
+                                            self._BACKENDS[stats], C.byref(self._h)))
+        self._cfg = cfg
+        self._n = n_envs
+        self.devices = list(devices)
+
+    def n_envs(self) -> int:
+        return self._n
+
+    def n_shards(self) -> int:
+        return int(self._lib.ut_multienv_n_shards(self._h))
+
+    def shard_range(self, i: int):
+        b, e, d = C.c_int64(), C.c_int64(), C.c_int32()
+        _check(self._lib.ut_multienv_shard(self._h, i, None, C.byref(b), C.byref(e), C.byref(d)))
+        return int(b.value), int(e.value), int(d.value)
+
+    def stats_backend(self) -> str:
+        return "nccl" if self._lib.ut_multienv_stats_backend(self._h) == _abi.UT_MULTI_STATS_NCCL else "host"
+
+    def reset_all(self):
+        _check(self._lib.ut_multienv_reset_all(self._h))
+
+    def step(self, actions):
+        a = np.ascontiguousarray(np.asarray(actions, np.int32).reshape(-1))
+        if a.size != self._n * self._cfg.n_agents:
+            raise ContractViolation("vecenv step: wrong action count")
+        _check(self._lib.ut_multienv_step(self._h, a.ctypes.data_as(C.c_void_p)))
+
+    def step_policy(self, policy="random", n_steps: int = 1):
+        _check(self._lib.ut_multienv_step_policy(self._h, _POLICIES[policy], n_steps))
+
+    def refresh_outputs(self):
+        _check(self._lib.ut_multienv_refresh_outputs(self._h))
+
+    def set_auto_reset(self, on: bool):
+        _check(self._lib.ut_multienv_set_auto_reset(self._h, int(on)))
+
+    def host_outputs(self, names=None):
+        """The whole batch's outputs, laid out like VecEnv.host_outputs()."""
+        n, A, T = self._n, self._cfg.n_agents, self._cfg.n_targets
+        R = A + T
+        shapes = {
+            "obs": ((kFeatureDim, n * A * R), np.float64), "final_obs": ((kFeatureDim, n * A * R), np.float64),
+            "global_state": ((kFeatureDim, n * R), np.float64), "rewards": ((n,), np.float64),
+            "dones": ((n,), np.uint8), "masks": ((n * A * kNumActions,), np.uint8),
+            "tracking_error": ((n * T,), np.float64), "min_agent_dist": ((n * T,), np.float64),
+            "target_lost": ((n * T,), np.uint8), "collision": ((n,), np.uint8), "step": ((n,), np.int32),
+        }
+        names = list(shapes) if names is None else list(names)
+        out = {k: np.empty(*shapes[k]) for k in names}
+        ho = _abi.HostOutputs(**{k: v.ctypes.data for k, v in out.items()})
+        _check(self._lib.ut_multienv_copy_outputs(self._h, C.byref(ho)))
+        return out
+
+    def stats(self, reset: bool = False) -> np.ndarray:
+        out = (C.c_double * _abi.UT_N_STATS)()
+        _check(self._lib.ut_multienv_stats(self._h, out, int(reset)))
+        return np.array(out[:])
+
+    def enable_phase_timing(self, on: bool = True):
+        _check(self._lib.ut_multienv_enable_phase_timing(self._h, int(on)))
+
+    def phase_ns(self, reset: bool = False) -> dict:
+        out = (C.c_uint64 * _abi.UT_N_PHASES)()
+        _check(self._lib.ut_multienv_phase_ns(self._h, out, int(reset)))
+        return dict(zip(_abi.PHASE_NAMES, out[:]))
+
+    def serialize_state(self, env: int) -> np.ndarray:
+        n = C.c_size_t()
+        _check(self._lib.ut_multienv_serialize(self._h, env, None, 0, C.byref(n)))
+        blob = np.empty(n.value, np.float64)
+        _check(self._lib.ut_multienv_serialize(self._h, env, blob.ctypes.data_as(C.POINTER(C.c_double)),
+                                               blob.size, C.byref(n)))
+        return blob
+
+    def deserialize_state(self, env: int, blob):
+        b = np.ascontiguousarray(blob, np.float64)
+        _check(self._lib.ut_multienv_deserialize(self._h, env, b.ctypes.data_as(C.POINTER(C.c_double)), b.size))
+
+    def world_step(self, env: int) -> int:
+        s = C.c_int32()
+        _check(self._lib.ut_multienv_world_step(self._h, env, C.byref(s)))
+        return int(s.value)
+
+    def launch_count(self) -> int:
+        return int(self._lib.ut_multienv_launch_count(self._h))
+
+    def synchronize(self):
+        _check(self._lib.ut_multienv_synchronize(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.ut_multienv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Environment:
     """One environment (env.hpp:91-171): a VecEnv shard holding the single global
     env ``env_index``, so its streams equal ``Environment(cfg, seed, env_index)``.

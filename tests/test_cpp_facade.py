@@ -51,3 +51,4 @@ def test_facade_matches_python_mirror(tmp_path, cuda_device):
     assert d["step0"] == v.world_step(0)
     assert d["blob"] == v.serialize_state(0).size
     assert d["all"] == 4 * d["blob"]
+    assert d["multi_same"] == 1  # ut::MultiVecEnv over two shards == ut::VecEnv
