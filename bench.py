@@ -124,6 +124,15 @@ class ClockSampler:
                  "-i", str(self.gpu)], stdout=self.fh, stderr=subprocess.DEVNULL)
         except (FileNotFoundError, OSError):
             self.proc = None
+            return self
+        # nvidia-smi takes ~0.1-0.5 s to produce its first line: wait for it, so
+        # even a sub-second timed region is sampled (the first sample is pre-load)
+        t0 = time.time()
+        while time.time() - t0 < 3.0 and self.proc.poll() is None:
+            if self.path.stat().st_size > 0:
+                break
+            time.sleep(0.02)
+        self.skip = sum(1 for _ in self.path.open()) if self.path.exists() else 0
         return self
 
     def __exit__(self, *exc):
@@ -140,7 +149,11 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.path.read_text().splitlines():
+        lines = self.path.read_text().splitlines()
+        skip = getattr(self, "skip", 0)
+        if len(lines) > skip:  # samples taken before the timed region started are dropped
+            lines = lines[skip:]
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
                 continue
@@ -427,7 +440,7 @@ def main():
         prev = t_one
     # windows of exactly K steps; short ones are repeated until ~1 s has been
     # timed so the clock sampler (200 ms period) sees the load (median window)
-    windows = max(1, min(50, int(1000.0 / max(prev or t_one, 1e-3) / max(1, args.steps)) + 1))
+    windows = max(1, min(5000, int(1000.0 / max(prev or t_one, 1e-3) / max(1, args.steps)) + 1))
     if world > 1:
         t_w = torch.tensor([windows], dtype=torch.int64, device="cuda")
         dist.all_reduce(t_w, op=dist.ReduceOp.MAX)

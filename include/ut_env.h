@@ -196,8 +196,11 @@ int ut_vecenv_reset_all(ut_vecenv* v);
  * nothing is mutated and UT_ERR_CONTRACT names the lowest failing env ("env i: ..."). */
 int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device);
 /* VecEnv::step_policy (vecenv.cpp:118-143), policy UT_POLICY_*. n_steps > 1 runs
- * that many steps back to back: one kernel launch each, no host round trip in
- * between; the status is checked once at the end. */
+ * that many steps back to back with no host round trip in between, as ONE CUDA
+ * graph launch of n_steps cooperative step kernels (captured on first use per
+ * (policy, n_steps), re-captured after any change to the handle's launch state;
+ * single output buffer only; UT_NO_GRAPHS=1 in the environment disables it);
+ * the status is checked once at the end. */
 int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps);
 /* VecEnv::refresh_outputs (vecenv.cpp:145-150). */
 int ut_vecenv_refresh_outputs(ut_vecenv* v);

@@ -6,7 +6,7 @@
  * IEEE op per source operation, no contraction (-ffp-contract=off), sequential
  * reductions, glibc fp64 libm, correctly-rounded fp32 log/sin/cos -- the same
  * definition as oracle/eigen_shim (so this file and oracle/_ref agree bit for bit,
- * tests/test_oracle_vs_ref.py).
+ * tests/test_oracle_pinning.py).
  *
  * Batch semantics follow VecEnv (vecenv.cpp) with one declared superset: the
  * self-driven step (step_policy) also refreshes obs/global/infos/final_obs, which

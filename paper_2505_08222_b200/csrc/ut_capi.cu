@@ -166,6 +166,8 @@ struct ut_vecenv {
       if (ev) cudaEventDestroy(ev);
     for (void* p : allocs) cudaFree(p);
     if (h_status) cudaFreeHost(h_status);
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     if (own_stream) cudaStreamDestroy(own_stream);
   }
 
@@ -231,6 +233,7 @@ struct ut_vecenv {
 
   // Publishes B to its device copy; call after any change to B.
   int sync_batch() {
+    ++batch_version;  // B is a kernel parameter: captured step graphs are stale now
     B.self = d_self;
     UT_CUDA(cudaMemcpyAsync(d_self, &B, sizeof(DevBatch), cudaMemcpyHostToDevice, stream));
     return UT_OK;
@@ -270,8 +273,93 @@ struct ut_vecenv {
     return UT_OK;
   }
 
+  // Multi-step step_policy as one CUDA graph of n cooperative step launches
+  // (launch-bound small batches such as C1: one graph launch instead of n
+  // kernel launches). The graph is captured on a private stream, launched on the
+  // handle's stream (which may be the legacy default stream, where capture is
+  // not allowed), and re-captured whenever B, the grid or (mode, n) change.
+  uint64_t batch_version = 0;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  int graph_mode = -1, graph_n = 0, graph_grid = 0;
+  uint64_t graph_version = 0;
+  bool graphs_off = getenv("UT_NO_GRAPHS") != nullptr;
+
+  int launch_kernel(int mode, cudaStream_t s) {
+    void (*kern)(DevBatch, int, int32_t*) = nullptr;
+    if (full && np == 1024)
+      kern = step_kernel<kPPT, 1024, true>;
+    else if (full && np == 512)
+      kern = step_kernel<kPPT, 512, true>;
+    else if (full && np == 256)
+      kern = step_kernel<kPPT, 256, true>;
+    else
+      kern = step_kernel<kPPT, 1024, false>;
+    // cooperative: the kernel's phases are separated by grid-wide barriers
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)grid);
+    lc.blockDim = dim3((unsigned)nt);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    UT_CUDA(cudaLaunchKernelEx(&lc, kern, B, mode, d_status));
+    UT_CUDA(cudaGetLastError());
+    return UT_OK;
+  }
+
+  // n_steps policy steps; true in *used when they went out as one graph launch
+  int launch_steps_graph(int mode, int n_steps, bool* used) {
+    *used = false;
+    if (graphs_off || n_out != 1 || n_steps < 2) return UT_OK;
+    if (!graph_exec || graph_mode != mode || graph_n != n_steps || graph_grid != grid ||
+        graph_version != batch_version) {
+      if (graph_exec) cudaGraphExecDestroy(graph_exec);
+      graph_exec = nullptr;
+      if (!cap_stream) UT_CUDA(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking));
+      UT_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeThreadLocal));
+      int rc = UT_OK;
+      for (int i = 0; i < n_steps && !rc; ++i) rc = launch_kernel(mode, cap_stream);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(cap_stream, &g);
+      if (rc || ce != cudaSuccess || !g) {
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();
+        graphs_off = true;  // capture unsupported here: plain launches from now on
+        return UT_OK;
+      }
+      const cudaError_t ie = cudaGraphInstantiate(&graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) {
+        cudaGetLastError();
+        graph_exec = nullptr;
+        graphs_off = true;
+        return UT_OK;
+      }
+      graph_mode = mode, graph_n = n_steps, graph_grid = grid, graph_version = batch_version;
+    }
+    int rc;
+    if ((rc = wait_outputs(cur))) return rc;
+    UT_CUDA(cudaGraphLaunch(graph_exec, stream));
+    launches += n_steps;
+    *used = true;
+    return UT_OK;
+  }
+
+  // n_steps policy steps back to back: one graph launch, else n kernel launches
+  int enqueue_policy_steps(int mode, int n_steps) {
+    bool graphed = false;
+    int rc;
+    if ((rc = launch_steps_graph(mode, n_steps, &graphed))) return rc;
+    for (int i = 0; i < n_steps && !graphed; ++i)
+      if ((rc = launch_step(mode))) return rc;
+    return UT_OK;
+  }
+
   int launch_step(int mode) {
-    const dim3 g((unsigned)grid), b((unsigned)nt);
     int rc;
     if (n_out == 2) {
       const int t = cur ^ 1;
@@ -284,29 +372,8 @@ struct ut_vecenv {
     } else if ((rc = wait_outputs(cur))) {
       return rc;
     }
-    void (*kern)(DevBatch, int, int32_t*) = nullptr;
-    if (full && np == 1024)
-      kern = step_kernel<kPPT, 1024, true>;
-    else if (full && np == 512)
-      kern = step_kernel<kPPT, 512, true>;
-    else if (full && np == 256)
-      kern = step_kernel<kPPT, 256, true>;
-    else
-      kern = step_kernel<kPPT, 1024, false>;
-    // cooperative: the kernel's phases are separated by grid-wide barriers
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = g;
-    lc.blockDim = b;
-    lc.dynamicSmemBytes = smem;
-    lc.stream = stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    UT_CUDA(cudaLaunchKernelEx(&lc, kern, B, mode, d_status));
+    if ((rc = launch_kernel(mode, stream))) return rc;
     ++launches;
-    UT_CUDA(cudaGetLastError());
     return UT_OK;
   }
   int launch_reset(int ctor) {
@@ -656,8 +723,7 @@ int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps) {
     return fail(UT_ERR_CONTRACT, "step_policy: unknown policy %d", policy);
   int rc;
   if ((rc = v->reset_status())) return rc;
-  for (int i = 0; i < n_steps; ++i)
-    if ((rc = v->launch_step(policy == UT_POLICY_RANDOM ? MODE_RANDOM : MODE_SCRIPTED))) return rc;
+  if ((rc = v->enqueue_policy_steps(policy == UT_POLICY_RANDOM ? MODE_RANDOM : MODE_SCRIPTED, n_steps))) return rc;
   return v->check_status("step_policy");
 }
 

@@ -241,9 +241,7 @@ int ut_multienv_step_policy(ut_multienv* m, int policy, int n_steps) {
   return each_shard_then_status(m, "step_policy", [&](ut_vecenv* v, size_t) -> int {
     int rc;
     if ((rc = v->reset_status())) return rc;
-    for (int s = 0; s < n_steps; ++s)
-      if ((rc = v->launch_step(mode))) return rc;
-    return UT_OK;
+    return v->enqueue_policy_steps(mode, n_steps);
   });
 }
 

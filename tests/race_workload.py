@@ -38,8 +38,8 @@ def _dbg():
 
 def make(kind):
     if kind == "c3":
-        cfg = EnvConfig(n_agents=5, n_targets=5, horizon=3, target_speed_frac=0.9, target_speed_frac_max=1.0,
-                        pf=PfConfig(n_particles=1024))
+        cfg = EnvConfig(n_agents=5, n_targets=5, horizon=3, target_speed_frac=0.6, d_min=100.0,
+                        spawn_max_sep=400.0, pf=PfConfig(n_particles=1024))  # bench.py CONFIGS["c3"]
         return VecEnv(cfg, 24, 5)
     cfgs = [EnvConfig(n_agents=a, n_targets=t, horizon=3, spawn_max_sep=600.0, pf=PfConfig(n_particles=1024),
                       **(HEAVY if h else {})) for a, t, h in MIX]

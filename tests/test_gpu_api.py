@@ -145,3 +145,28 @@ def test_phase_timing_covers_the_reference_phases(cuda_device):
     rep = benchmark_sps(cfg, 256, 4, warmup=2)
     assert rep["phase_ns"]["filter"] > 0 and rep["total_ns"] == sum(
         rep["phase_ns"][k] for k in ("targets", "agents", "measure", "filter", "comms", "observe", "reward"))
+
+
+def test_multi_step_graph_equals_single_launches(cuda_device):
+    """step_policy(n > 1) goes out as one CUDA graph of n cooperative launches
+    (re-captured after a change to the launch state): the same batch as n
+    single-step calls, across an auto-reset and an output-buffer switch."""
+    from paper_2505_08222_b200.vecenv import VecEnv
+    from test_gpu_parity import _to_py
+    cfg = _to_py(default_config(n_agents=2, n_targets=2, pf_n_particles=1024, horizon=4))
+    a, b = VecEnv(cfg, 33, 4), VecEnv(cfg, 33, 4)
+    for policy, n in (("random", 3), ("scripted", 5), ("random", 3)):
+        n0 = a.launch_count()
+        a.step_policy(policy, n)
+        assert a.launch_count() - n0 == n
+        for _ in range(n):
+            b.step_policy(policy, 1)
+        assert np.array_equal(a.export_state(), b.export_state())
+        ha, hb = a.host_outputs(), b.host_outputs()
+        assert all(np.array_equal(ha[k], hb[k]) for k in ha)
+    a.enable_phase_timing(True)  # changes the kernel parameters: the graph is re-captured
+    b.enable_phase_timing(True)
+    a.step_policy("random", 3)
+    for _ in range(3):
+        b.step_policy("random", 1)
+    assert np.array_equal(a.export_state(), b.export_state())
