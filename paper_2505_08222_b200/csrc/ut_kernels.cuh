@@ -38,7 +38,7 @@ constexpr int kMaxEntities = 64;  // spawn scratch per thread
 constexpr double kMergeFloor = 0x1p-860;  // see the merged-update argument in step_set
 constexpr int kChunkFlagDone = 1, kChunkFlagSpawned = 2;
 constexpr int kBcStatUpdates = 8, kBcStatResamples = 9, kBcStatExact = 10;  // Smem::bc slots
-constexpr int kBcClaim = 11;  // the filter phase's next env (int)
+constexpr int kBcClaim = 11;  // the filter phase's claimed envs (int), two slots used in turn
 
 // Strided view of one env's record: word w at p[w * n_envs].
 struct Rec {
@@ -1225,17 +1225,22 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     ut_bar();
     double shift = 0.0;  // sum_j s'_j, in stage order
     const uint32_t* mbu = reinterpret_cast<const uint32_t*>(mb);
-    for (int j = 0; j < nm; ++j) {
-      uint32_t hj = mbu[j * 32];
+    // lane j < nm combines stage j's warp maxima once; the stage-order sum then
+    // takes them lane by lane (the same operands in the same order)
+    uint32_t hl = 0xFFFFFFFFu;
+    if (lane < nm) {
       if constexpr (NW > 0 && NW % 4 == 0) {
 #pragma unroll
         for (int v = 0; v < NW; v += 4) {
-          const uint4 m4 = *reinterpret_cast<const uint4*>(mbu + j * 32 + v);
-          hj = min(hj, min(min(m4.x, m4.y), min(m4.z, m4.w)));
+          const uint4 m4 = *reinterpret_cast<const uint4*>(mbu + lane * 32 + v);
+          hl = min(hl, min(min(m4.x, m4.y), min(m4.z, m4.w)));
         }
       } else {
-        for (int v = 1; v < nw; ++v) hj = min(hj, mbu[j * 32 + v]);
+        for (int v = 0; v < nw; ++v) hl = min(hl, mbu[lane * 32 + v]);
       }
+    }
+    for (int j = 0; j < nm; ++j) {
+      const uint32_t hj = __shfl_sync(0xffffffffu, hl, j);
       const double sj = __hiloint2double((int)hj, 0);  // >= max_i ll_ij
       shift = j == 0 ? sj : shift + sj;
     }
@@ -1247,7 +1252,6 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       }
     } else {
       double e[PPT], ls = 0.0, lq = 0.0;
-      int lx = 0;  // max biased exponent of e
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         e[q] = 0.0;
@@ -1255,7 +1259,6 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           e[q] = s.w[q] * exp_neg(L[q] - shift, S.tab_exp);
           ls = ls + e[q];
           lq = lq + e[q] * e[q];
-          lx = max(lx, __double2hiint(e[q]) >> 20);
         }
       }
       if (merged) {  // before the barrier after which the staging may start
@@ -1263,16 +1266,20 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         load_field<PPT>(S.pf + 3 * NPf, k0, s.vy);
       }
       SETPROF(4);
-      const double2 r = R.sum2_imax<NW>(ls, lq, lx);
+      // the guards on max(e) from the sum: sum >= 2^-850 gives max >= sum / P >=
+      // 2^-860 (P <= 1024), sum >= 2^-190 gives max >= 2^-200
+      const double2 r = R.sum2<NW>(ls, lq);
       SETPROF(5);
-      if (isfinite(r.x) && r.x > 0.0 && lx >= 1023 - 860) {  // max(e) >= 2^-860
-        // r.x in [2^-860, P] and r.x^2, r.y >= 2^-400 where the ESS is formed:
+      const bool guard_ok = isfinite(r.x) && r.x >= 0x1p-850;
+      const bool ess_ok = r.x >= 0x1p-190;
+      if (guard_ok) {
+        // r.x in [2^-850, P] and r.x^2, r.y >= 2^-400 where the ESS is formed:
         // the branch-free IEEE divisions apply
         const double rcp = div_rn_clamp(1.0, r.x);
 #pragma unroll
         for (int q = 0; q < PPT; ++q) s.w[q] = div_rcp(e[q], r.x, rcp);
         // ESS = sum^2 / sum(e^2) unless the squares may have underflowed
-        if (lx >= 1023 - 200) {
+        if (ess_ok) {
           ess = div_rn_clamp(r.x * r.x, r.y);
           have_ess = true;
         }
@@ -1621,19 +1628,25 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
   ph_mark(B, kPhaseWait);
   // ---- 2. particle sets, env by env from the work counter; the next env is
   // claimed at the start of the current one so its first set can be prefetched
+  // The claims alternate between two slots: a slot is rewritten two claims
+  // later, after barriers every thread has passed since reading it (thread 0
+  // writes the next claim right after stage_env, which has no barrier, so one
+  // slot would let it overwrite a claim a late warp has not read yet).
   int* claim = reinterpret_cast<int*>(S.bc + kBcClaim);
+  int slot = 0;
   if (threadIdx.x == 0) {
     const int e = atomicAdd(B.work, 1);
-    *claim = e;
+    claim[0] = e;
     if (FULL && e < n) prefetch_set(B, S, set_off(B, e), B.P);
   }
   ut_bar();
-  int e = *claim;
+  int e = claim[0];
   while (e < n) {
     stage_env(cfg_of(B, e), B, S, rec_of(B, e), e);
-    if (threadIdx.x == 0) *claim = atomicAdd(B.work, 1);
+    slot ^= 1;
+    if (threadIdx.x == 0) claim[slot] = atomicAdd(B.work, 1);
     ut_bar();
-    const int en = *claim;
+    const int en = claim[slot];
     const DevConfig& c = *S.cfg;
     const int so = (int)set_off(B, e);
     const int nA = c.A, nT = c.T;

@@ -25,6 +25,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2505_08222_b200 import _abi, _native  # noqa: E402
 from paper_2505_08222_b200.vecenv import EnvConfig, PfConfig, VecEnv  # noqa: E402
 
+VERBOSE = False
 HEAVY = dict(comm_drop_prob=0.0, detection_range=1e9, comm_range=1e9)
 MIX = [(8, 8, True), (1, 1, False), (3, 5, False), (5, 3, False), (8, 1, True), (2, 7, False), (5, 5, True),
        (4, 4, False)]
@@ -67,6 +68,8 @@ def run(kind, grid):
         if s == 4:
             assert lib.ut_debug_set_knobs(v._h, 0, -1) == 0
         out[f"s{s}_blobs"] = v.export_state()
+        if VERBOSE:
+            print(f"{kind} grid {grid} step {s} ok", flush=True)
     v.refresh_outputs()
     for k, a in v.host_outputs().items():
         out[f"out_{k}"] = a
@@ -79,7 +82,10 @@ def run(kind, grid):
 
 
 def main():
-    path, grids = sys.argv[1], [int(g) for g in sys.argv[2:]]
+    global VERBOSE
+    args = [a for a in sys.argv[1:] if a != "-v"]
+    VERBOSE = len(args) != len(sys.argv) - 1
+    path, grids = args[0], [int(g) for g in args[1:]]
     res = {}
     for kind in ("c3", "c4"):
         for g in grids:

@@ -41,7 +41,11 @@ def main():
         if r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
             sys.exit(1)
-        regs = [ln for ln in r.stdout.splitlines() + r.stderr.splitlines() if "step_kernelILi4ELi1024ELb1" in ln]
+        lines = r.stdout.splitlines() + r.stderr.splitlines()
+        for i, ln in enumerate(lines):  # the FULL P = 1024 step kernel's registers / spills
+            if "Function properties for _ZN2ut11step_kernelILi4ELi1024ELb1" in ln:
+                print("  ", " | ".join(x.strip() for x in lines[i + 1:i + 3]))
+                break
     print(out)
 
 
