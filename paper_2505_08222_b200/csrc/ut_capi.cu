@@ -1332,6 +1332,12 @@ __global__ void ieee_check_kernel(int kind, uint64_t seed, int64_t n, unsigned l
       const double x = i == 0 ? 0.0 : exp2(-960.0 + 1160.0 * u) * (1.0 + v);
       const double a = sqrt_rn_clamp(x), b = __dsqrt_rn(x);
       local += __double_as_longlong(a) != __double_as_longlong(b);
+    } else if (kind == 2 || kind == 3) {
+      // the likelihood distance sqrt (sqrt_dist) against IEEE over squared
+      // distances up to (40 km)^2 (2: results more than 1 ulp off; 3: any difference)
+      const double x = i == 0 ? 0.0 : exp2(-60.0 + 91.0 * u) * (1.0 + v);
+      const long long a = __double_as_longlong(sqrt_dist(x)), b = __double_as_longlong(__dsqrt_rn(x));
+      local += kind == 3 ? a != b : (a - b > 1 || b - a > 1);
     } else {
       const double a = exp2(-20.0 + 40.0 * u);
       const double b = a * (1.0 + 1e6 * v);

@@ -1345,11 +1345,13 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     // 256-bit stores (STG.E.ENL2.256): one per field and 4 particles
 #pragma unroll
     for (int q = 0; q < PPT; q += 4) {
-      st_global_v4(B.px + base + k0 + q, s.px[q], s.px[q + 1], s.px[q + 2], s.px[q + 3]);
-      st_global_v4(B.py + base + k0 + q, s.py[q], s.py[q + 1], s.py[q + 2], s.py[q + 3]);
+      // the fields the estimate does not read first: their registers, freed
+      // first, are the ones the estimate's temporaries get
       st_global_v4(B.vx + base + k0 + q, s.vx[q], s.vx[q + 1], s.vx[q + 2], s.vx[q + 3]);
       st_global_v4(B.vy + base + k0 + q, s.vy[q], s.vy[q + 1], s.vy[q + 2], s.vy[q + 3]);
       st_global_v4(B.w + base + k0 + q, s.w[q], s.w[q + 1], s.w[q + 2], s.w[q + 3]);
+      st_global_v4(B.px + base + k0 + q, s.px[q], s.px[q + 1], s.px[q + 2], s.px[q + 3]);
+      st_global_v4(B.py + base + k0 + q, s.py[q], s.py[q + 1], s.py[q + 2], s.py[q + 3]);
     }
   } else {
 #pragma unroll
@@ -1510,11 +1512,13 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
   if constexpr (FULL) {
 #pragma unroll
     for (int q = 0; q < PPT; q += 4) {
-      st_global_v4(B.px + base + k0 + q, s.px[q], s.px[q + 1], s.px[q + 2], s.px[q + 3]);
-      st_global_v4(B.py + base + k0 + q, s.py[q], s.py[q + 1], s.py[q + 2], s.py[q + 3]);
+      // the fields the estimate does not read first: their registers, freed
+      // first, are the ones the estimate's temporaries get
       st_global_v4(B.vx + base + k0 + q, s.vx[q], s.vx[q + 1], s.vx[q + 2], s.vx[q + 3]);
       st_global_v4(B.vy + base + k0 + q, s.vy[q], s.vy[q + 1], s.vy[q + 2], s.vy[q + 3]);
       st_global_v4(B.w + base + k0 + q, s.w[q], s.w[q + 1], s.w[q + 2], s.w[q + 3]);
+      st_global_v4(B.px + base + k0 + q, s.px[q], s.px[q + 1], s.px[q + 2], s.px[q + 3]);
+      st_global_v4(B.py + base + k0 + q, s.py[q], s.py[q + 1], s.py[q + 2], s.py[q + 3]);
     }
   } else {
 #pragma unroll
