@@ -293,6 +293,16 @@ def test_speed_clamp_arithmetic_is_ieee(cuda_device, kind):
     assert bad.value == 0
 
 
+def test_likelihood_distance_sqrt_within_one_ulp(cuda_device):
+    """The likelihood distance sqrt (sqrt_dist: rsqrt seed, one Goldschmidt step,
+    residual correction) is within 1 ulp of IEEE on 2^28 squared distances; only
+    the particle weights use it (weights carry rounding anyway)."""
+    lib = _product()
+    bad = C.c_uint64(1)
+    assert lib.ut_debug_ieee_check(2, 4242, 1 << 28, 0, C.byref(bad)) == 0
+    assert bad.value == 0
+
+
 def test_batched_state_export_import(cuda_device):
     """ut_vecenv_export_state / import_state (checkpoint path) ==
     per-env serialize / deserialize, bit for bit, and an import restores state."""
