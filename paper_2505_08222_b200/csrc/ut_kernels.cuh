@@ -65,12 +65,12 @@ struct Smem {
   DevConfig* cfg;    // config of the env being filtered
   double* red;       // kRedDoubles: BlockReducer buffers + scan warp sums
   double* bc;        // 16 broadcast slots (0: resample draw; kBcStat*: the env's filter statistics)
-  uint4* xch;        // [32 warps][5] lane-0 Philox blocks (misaligned streams)
   double* meas;      // [sA*sT][kMeasStride] pings of the env being filtered
   uint16_t* mcount;  // [sA*sT] measurements applied to each set this step
   uint16_t* mlist;   // [sA*sT][sA] their meas indices in application order
   double* trk;       // [sA*sT][kTrkStride] the sets' track scalars + PF stream keys
   uint8_t* flags;    // [blockDim] per-env chunk flags
+  uint4* bnd;        // [A*T][4 nw + 2] the env's warp-boundary Philox blocks (stage_bnd)
   uint64_t* mbar;    // TMA completion barrier
   uint32_t mbar_sa, pf_sa;  // their shared-window addresses (computed once)
   double* pf;        // [5][P] TMA-prefetched next particle set
@@ -91,7 +91,6 @@ struct FixedSmem {
   double tab_exp[32];
   double red[kRedDoubles];
   double bc[16];
-  uint4 xch[32 * 5];
   uint64_t mbar[2];
   // phase timers (thread 0): the phases, barrier waits, the running section's
   // start, and the launch's start clock / globaltimer. Kept in the dynamic
@@ -106,6 +105,11 @@ struct FixedSmem {
   DevConfig cfg;
 };
 
+// Philox blocks of one set's noise that a warp's lanes do not cover themselves
+// (stage_bnd): for each of the 4 segments, the block after each warp's range;
+// then the two blocks holding the resample draw.
+__host__ __device__ constexpr int bnd_per_set(int nw) { return 4 * nw + 2; }
+
 template <int NP>
 __host__ __device__ inline size_t smem_bytes(int sA, int sT, int nt) {
   size_t s = align16(sizeof(FixedSmem<NP>));
@@ -114,6 +118,7 @@ __host__ __device__ inline size_t smem_bytes(int sA, int sT, int nt) {
   s += align16(sizeof(uint16_t) * sA * sT * sA);
   s += align16(sizeof(double) * kTrkStride * sA * sT);
   s += align16(nt);
+  s += sizeof(uint4) * sA * sT * bnd_per_set(nt / 32);
   return s;
 }
 
@@ -127,7 +132,6 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int sA, int sT) {
   S.cfg = &F.cfg;
   S.red = F.red;
   S.bc = F.bc;
-  S.xch = F.xch;
   S.mbar = F.mbar;
   S.mbar_sa = smem_addr(F.mbar);
   S.pf_sa = smem_addr(F.pf);
@@ -144,6 +148,8 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int sA, int sT) {
   S.trk = (double*)(base + o);
   o += align16(sizeof(double) * kTrkStride * sA * sT);
   S.flags = base + o;
+  o += align16(blockDim.x);
+  S.bnd = reinterpret_cast<uint4*>(base + o);
   return S;
 }
 
@@ -1006,36 +1012,30 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // NB = PPT/4 aligned blocks pos/4 + s*P/4 + NB*t + i of each segment; a
   // misaligned stream takes its remaining words from the next lane's first
   // block (shuffle). Lane 31 needs the block after its warp's range in each
-  // segment: lanes 0..3 of every warp compute those four as one more,
-  // interleaved chain (so no warp waits for another) and hand them over through
-  // the warp's xch slots. The last warp's segment-3 extra block, pos/4 + P, also
-  // holds the resample draw at pos + 4P.
+  // segment: stage_bnd computed those (and the resample draw's blocks) for
+  // every set of the env at once, spread over the whole CTA.
   constexpr int NB = PPT / 4 > 0 ? PPT / 4 : 1;
   uint4 blk[4][NB];
+  const uint4* bnd = S.bnd + ps * bnd_per_set(nw);
   if (FULL && noise) {
-    uint64_t bq[4 * NB + 1];
+    uint64_t bq[4 * NB];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int i = 0; i < NB; ++i)
         bq[q * NB + i] = (pos >> 2) + (uint64_t)q * (uint64_t)(P / 4) + (uint64_t)(NB * tid + i);
-    bq[4 * NB] = (pos >> 2) + (uint64_t)(lane & 3) * (uint64_t)(P / 4) + (uint64_t)(NB * 32 * (warp + 1));
-    uint4 bo[4 * NB + 1];
-    philox_n<4 * NB + 1>(key, (uint64_t)ps, bq, bo);
+    uint4 bo[4 * NB];
+    philox_n<4 * NB>(key, (uint64_t)ps, bq, bo);
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int i = 0; i < NB; ++i) blk[q][i] = bo[q * NB + i];
-    const uint4 ex = bo[4 * NB];
-    st_shared_if(lane < 4, S.xch + warp * 5 + (lane & 3), ex);
     if (warp == nw - 1 && lane == 3) {
-      const uint4 y = off == 3 ? philox(key, (uint64_t)ps, (pos >> 2) + (uint64_t)P + 1) : ex;
       uint32_t w2[4];
-      words_at(ex, y, off, w2);
+      words_at(bnd[4 * nw], bnd[4 * nw + 1], off, w2);
       reinterpret_cast<uint32_t*>(S.bc)[0] = w2[0];
       reinterpret_cast<uint32_t*>(S.bc)[1] = w2[1];
     }
-    __syncwarp();
   } else if (tid == 0) {  // the resample draw, broadcast through smem
     const uint4 x = philox(key, (uint64_t)ps, u0p >> 2);
     const int o = (int)(u0p & 3);
@@ -1061,7 +1061,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         nb.x = __shfl_down_sync(0xffffffffu, blk[q][0].x, 1);
         nb.y = __shfl_down_sync(0xffffffffu, blk[q][0].y, 1);
         nb.z = __shfl_down_sync(0xffffffffu, blk[q][0].z, 1);
-        const uint4 xq = S.xch[warp * 5 + q];  // broadcast load, selected on lane 31
+        const uint4 xq = bnd[q * nw + warp];  // broadcast load, selected on lane 31
         if (off != 0 && lane == 31) nb = xq;
         uint32_t a[4 * NB + 3];
 #pragma unroll
@@ -1392,6 +1392,44 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   SETPROF(10);
 }
 
+// The warp-boundary Philox blocks of every set of the staged env (the FULL
+// instance's noise, step_set): per set, for each segment q and warp w the block
+// pos/4 + q P/4 + NB 32 (w + 1), then pos/4 + P and pos/4 + P + 1 (the resample
+// draw at pos + 4P). Spread over the whole CTA as 4 interleaved chains per
+// thread, once per env, instead of a fifth chain in every thread of every set.
+// Needs the env's staged track scalars (S.trk); caller syncs before and after.
+template <int PPT>
+__device__ __noinline__ void stage_bnd(const DevConfig& c, const Smem& S) {
+  constexpr int NB = PPT / 4 > 0 ? PPT / 4 : 1;
+  const int nw = blockDim.x >> 5, per = bnd_per_set(nw), P = c.P;
+  const int total = c.A * c.T * per;
+  for (int i0 = threadIdx.x; i0 < total; i0 += 4 * blockDim.x) {
+    uint32_t c0[4], c1[4], c2[4], c3[4], k0[4], k1[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int item = min(i0 + j * (int)blockDim.x, total - 1);
+      const int ps = item / per, r = item - ps * per;
+      const int a = ps / c.T, t = ps - a * c.T;
+      const double* tk = S.trk + kTrkStride * (a * c.sT + t);
+      const uint64_t pos = (uint64_t)tk[TK_POS];
+      const uint64_t key = (uint64_t)__double_as_longlong(tk[TK_KEY]);
+      const int q = r / nw, w = r - q * nw;
+      const uint64_t blk = r < 4 * nw
+                               ? (pos >> 2) + (uint64_t)q * (uint64_t)(P / 4) + (uint64_t)(NB * 32 * (w + 1))
+                               : (pos >> 2) + (uint64_t)P + (uint64_t)(r - 4 * nw);
+      c0[j] = (uint32_t)blk, c1[j] = (uint32_t)(blk >> 32);
+      c2[j] = (uint32_t)ps, c3[j] = 0u;
+      k0[j] = (uint32_t)key, k1[j] = (uint32_t)(key >> 32);
+    }
+    philox_keys<4>(c0, c1, c2, c3, k0, k1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int item = i0 + j * (int)blockDim.x;
+      if (item < total) S.bnd[item] = make_uint4(c0[j], c1[j], c2[j], c3[j]);
+    }
+  }
+}
+
 // Stage env e's config and ping schedule for the particle phase: measurement
 // rows and the per-set update lists (own ping, then senders in ascending order).
 // Caller syncs.
@@ -1652,6 +1690,10 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
     ut_bar();
     const int en = claim[slot];
     const DevConfig& c = *S.cfg;
+    if (FULL) {
+      stage_bnd<PPT>(c, S);
+      ut_bar();
+    }
     const int so = (int)set_off(B, e);
     const int nA = c.A, nT = c.T;
     const int first_next = en < n ? (int)set_off(B, en) : -1;
