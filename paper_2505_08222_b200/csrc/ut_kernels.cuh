@@ -1430,6 +1430,32 @@ __device__ __noinline__ void stage_bnd(const DevConfig& c, const Smem& S) {
   }
 }
 
+// L2 prefetch of the record words and ping schedule stage_env will read for env
+// e (one address per thread), issued an env ahead so the staging's scattered
+// loads (one 32-B sector per word of the structure-of-arrays record) hit L2.
+__device__ __forceinline__ void prefetch_env(const DevBatch& B, int64_t e) {
+  const DevConfig& c = cfg_of(B, e);
+  const int A = c.A, T = c.T, i = threadIdx.x;
+  const double* p = nullptr;
+  if (i < A) {
+    p = B.rec + (int64_t)(c.o_agent + V_X * c.sA + i) * B.n_envs + e;
+  } else if (i < 2 * A) {
+    p = B.rec + (int64_t)(c.o_agent + V_Y * c.sA + (i - A)) * B.n_envs + e;
+  } else if (i < 2 * A + 7 * A * T) {
+    const int j = i - 2 * A, f = j / (A * T), s = j - f * (A * T), a = s / T, t = s - a * T;
+    // the staged fields K_POS, K_MAXSPEED, K_EX, K_EY, K_ESSOK, K_AGE, K_EVER as 4-bit codes
+    constexpr uint32_t kF = K_POS | K_MAXSPEED << 4 | K_EX << 8 | K_EY << 12 | K_ESSOK << 16 | K_AGE << 20 |
+                            K_EVER << 24;
+    const int fld = (int)((kF >> (4 * f)) & 15u);
+    p = B.rec + (int64_t)(c.o_track + fld * c.sA * c.sT + a * c.sT + t) * B.n_envs + e;
+  } else if (i == 2 * A + 7 * A * T) {
+    p = B.sched_r2 + e * (int64_t)(c.sA * c.sT);
+  } else if (i == 2 * A + 7 * A * T + 1) {
+    p = reinterpret_cast<const double*>(B.sched_flags + e * (int64_t)(c.sA * c.sT + c.sA * c.sA));
+  }
+  if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // Stage env e's config and ping schedule for the particle phase: measurement
 // rows and the per-set update lists (own ping, then senders in ascending order).
 // Caller syncs.
@@ -1684,12 +1710,16 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
   ut_bar();
   int e = claim[0];
   while (e < n) {
+    // the next claim goes out first: its round trip overlaps the staging loads
+    int nxt = 0;
+    if (threadIdx.x == 0) nxt = atomicAdd(B.work, 1);
     stage_env(cfg_of(B, e), B, S, rec_of(B, e), e);
     slot ^= 1;
-    if (threadIdx.x == 0) claim[slot] = atomicAdd(B.work, 1);
+    if (threadIdx.x == 0) claim[slot] = nxt;
     ut_bar();
     const int en = claim[slot];
     const DevConfig& c = *S.cfg;
+    if (en < n) prefetch_env(B, en);  // its staging loads hit L2 when its turn comes
     if (FULL) {
       stage_bnd<PPT>(c, S);
       ut_bar();
@@ -1705,11 +1735,13 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
       }
     ut_bar();  // S.cfg / meas / mlist / claim reused by the next env
     if (threadIdx.x == 0) {  // the env's filter statistics, accumulated in smem per set
+      // fire-and-forget reductions (this CTA is the env's only writer): warp 0
+      // goes on to the next env's staging without waiting for the loads of +=
       const DevConfig& cg = cfg_of(B, e);
       double* st = B.rec + e + (int64_t)cg.o_stats * B.n_envs;
-      st[7 * B.n_envs] += S.bc[kBcStatUpdates];
-      st[8 * B.n_envs] += S.bc[kBcStatResamples];
-      st[9 * B.n_envs] += S.bc[kBcStatExact];
+      atomicAdd(st + 7 * B.n_envs, S.bc[kBcStatUpdates]);
+      atomicAdd(st + 8 * B.n_envs, S.bc[kBcStatResamples]);
+      atomicAdd(st + 9 * B.n_envs, S.bc[kBcStatExact]);
     }
     e = en;
   }
