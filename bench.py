@@ -554,6 +554,7 @@ def main():
     # after each step; the rest of that step's outputs is copied on a side stream
     # while the next step runs (ut_vecenv_copy_outputs_async).
     venv.set_output_buffers(2)
+    venv.set_stream(None)  # the handle's own non-blocking stream, as a default VecEnv runs
     copy_stream = torch.cuda.Stream()
     rest = {k: v for k, v in host.items() if k != "masks"}
     venv.copy_outputs_into({"masks": host["masks"]})

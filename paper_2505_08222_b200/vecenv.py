@@ -465,9 +465,13 @@ class VecEnv:
     def launch_count(self) -> int:
         return int(self._lib.ut_vecenv_launch_count(self._h))
 
-    def set_stream(self, stream_ptr: int):
+    def set_stream(self, stream_ptr):
         """Run on a caller's CUDA stream; 0 is the legacy default stream (torch's
-        default), passed to the library as UT_STREAM_LEGACY."""
+        default), passed to the library as UT_STREAM_LEGACY; None returns to the
+        handle's own non-blocking stream."""
+        if stream_ptr is None:
+            _check(self._lib.ut_vecenv_set_stream(self._h, None))
+            return
         s = stream_ptr if stream_ptr else _abi.UT_STREAM_LEGACY
         _check(self._lib.ut_vecenv_set_stream(self._h, C.c_void_p(s)))
 
