@@ -532,8 +532,15 @@ def main():
         dist.all_reduce(st)
     st = st.cpu().numpy()
 
-    # ---- e2e through the public API with host buffers (pinned), copies timed
+    # ---- e2e through the public API with host buffers (pinned), copies timed.
+    # The step cost depends on the episode step (pings and resamples thin out as
+    # the targets run), so the e2e steps start where the timed window started:
+    # a fresh reset, then the same warm-up and settle steps (untimed).
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 10)
+    if e2e_steps:
+        venv.reset_all()
+        venv.step_policy("random", args.warmup + settle_steps)
+        torch.cuda.synchronize()
     n_loc = hi - lo
     Am, Rm, Tm = venv.n_agents(), venv.n_rows(), venv.n_targets()
     acts_h = torch.empty((n_loc, Am), dtype=torch.int32, pin_memory=True)
@@ -590,11 +597,21 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    split = {"host_policy": 0.0, "step_call": 0.0, "masks_d2h": 0.0, "async_enqueue": 0.0}
     for _ in range(e2e_steps):
+        ta = time.perf_counter()
         host_policy(host["masks"].numpy().reshape(-1, 5))
+        tb = time.perf_counter()
         venv.step(acts_h)
+        tc = time.perf_counter()
         venv.copy_outputs_into({"masks": host["masks"]})
+        td = time.perf_counter()
         venv.copy_outputs_async(rest, copy_stream.cuda_stream)
+        te_ = time.perf_counter()
+        split["host_policy"] += tb - ta
+        split["step_call"] += tc - tb
+        split["masks_d2h"] += td - tc
+        split["async_enqueue"] += te_ - td
     copy_stream.synchronize()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -629,10 +646,13 @@ def main():
                        settle_steps=settle_steps, timed_windows=windows,
                        window_ms=[round(x, 4) for x in times]),
         "e2e": {"value": e2e_value, "unit": "agent-env steps/s", "h2d_bytes_per_step": h2d,
+                "ms_per_step_split": {k: 1e3 * v / max(1, e2e_steps) for k, v in split.items()},
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "path": "VecEnv.step(host int32 actions from a host policy on the returned masks) + every output "
                         "to pinned host (ut_vecenv_step, ut_vecenv_copy_outputs for the masks, "
-                        "ut_vecenv_copy_outputs_async for the rest, overlapping the next step)"},
+                        "ut_vecenv_copy_outputs_async for the rest, overlapping the next step); the e2e "
+                        "steps start at the episode step the timed window starts at (reset + the same "
+                        "warm-up and settle steps), on the handle's own stream"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
                      "traffic": counts.get("dram_bytes_per_launch"),

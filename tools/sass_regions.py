@@ -50,7 +50,7 @@ def region_table():
         ("set: store to HBM", find("// ---- the set back to HBM", s0)),
         ("set: estimate + track record", find("// ---- estimate (env.cpp:403-407)", s0)),
     ]
-    end = find("// Stage env e's config and ping schedule", s0) - 1
+    end = next(i + 1 for i in range(s0, len(lines)) if lines[i] == "}")  # step_set's closing brace
     regs = []
     for i, (name, a) in enumerate(marks):
         b = marks[i + 1][1] - 1 if i + 1 < len(marks) else end
@@ -60,6 +60,8 @@ def region_table():
         ("pf_estimate", find("__device__ __forceinline__ double3 pf_estimate("), None),
         ("pf_resample", find("__device__ void pf_resample("), None),
         ("stage_env", find("__device__ __forceinline__ void stage_env("), None),
+        ("stage_bnd (boundary Philox blocks)", find("void stage_bnd("), None),
+        ("prefetch_env", find("void prefetch_env("), None),
         ("reinit (auto-reset PF)", find("__device__ __forceinline__ void reinit_particle("), None),
         ("step_kernel body", find("__global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel("), None),
         ("env_prologue", find("__device__ __noinline__ void env_prologue("), None),
