@@ -1239,10 +1239,15 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         for (int v = 0; v < nw; ++v) hl = min(hl, mbu[lane * 32 + v]);
       }
     }
-    for (int j = 0; j < nm; ++j) {
-      const uint32_t hj = __shfl_sync(0xffffffffu, hl, j);
-      const double sj = __hiloint2double((int)hj, 0);  // >= max_i ll_ij
-      shift = j == 0 ? sj : shift + sj;
+    // the sum over lanes 0..7 (nm <= kMaxMerged = 8) by an xor butterfly (every
+    // lane of the group ends with the same operands in the same pairing), then
+    // lane 0's total to the warp
+    {
+      double sj = lane < nm ? __hiloint2double((int)hl, 0) : 0.0;  // >= max_i ll_ij
+      sj = sj + __shfl_xor_sync(0xffffffffu, sj, 4);
+      sj = sj + __shfl_xor_sync(0xffffffffu, sj, 2);
+      sj = sj + __shfl_xor_sync(0xffffffffu, sj, 1);
+      shift = __shfl_sync(0xffffffffu, sj, 0);
     }
     if (!isfinite(shift)) {
       exact = true;
