@@ -1332,6 +1332,13 @@ __global__ void ieee_check_kernel(int kind, uint64_t seed, int64_t n, unsigned l
       const double x = i == 0 ? 0.0 : exp2(-960.0 + 1160.0 * u) * (1.0 + v);
       const double a = sqrt_rn_clamp(x), b = __dsqrt_rn(x);
       local += __double_as_longlong(a) != __double_as_longlong(b);
+    } else if (kind == 4) {
+      // the particle-weight exp (exp_neg, table in global memory here) against
+      // libm exp over [-760, 0]: results more than 1 ulp off
+      const double* tab = kExp2Tab;
+      const double x = -760.0 * u;
+      const long long a = __double_as_longlong(exp_neg(x, tab)), b = __double_as_longlong(exp(x));
+      local += (a - b > 1 || b - a > 1);
     } else if (kind == 2 || kind == 3) {
       // the likelihood distance sqrt (sqrt_dist) against IEEE over squared
       // distances up to (40 km)^2 (2: results more than 1 ulp off; 3: any difference)
