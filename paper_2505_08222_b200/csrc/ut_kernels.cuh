@@ -762,7 +762,8 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
         const double dx = s.px[j] - cx, dy = s.py[j] - cy;
         a0 = a0 + dx;
         a1 = a1 + dy;
-        a2 = a2 + (dx * dx + dy * dy);
+        a2 = fma(dx, dx, a2);
+        a2 = fma(dy, dy, a2);
       }
     }
   } else {
@@ -1282,7 +1283,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         // the branch-free IEEE divisions apply
         const double rcp = div_rn_clamp(1.0, r.x);
 #pragma unroll
-        for (int q = 0; q < PPT; ++q) s.w[q] = div_rcp(e[q], r.x, rcp);
+        // (e / sum to ~1 ulp: the merged weights carry the rounding of the tree
+        // sums and of exp anyway; the resample's strata see 1e-16 either way)
+        for (int q = 0; q < PPT; ++q) s.w[q] = e[q] * rcp;
         // ESS = sum^2 / sum(e^2) unless the squares may have underflowed
         if (ess_ok) {
           ess = div_rn_clamp(r.x * r.x, r.y);
