@@ -439,17 +439,25 @@ def main():
             break
         prev = t_one
     # windows of exactly K steps; short ones are repeated until ~1 s has been
-    # timed so the clock sampler (200 ms period) sees the load (median window)
+    # timed so the clock sampler (200 ms period) sees the load (median window);
+    # each repeat starts at the same episode step (reset + the same warm-up)
     windows = max(1, min(5000, int(1000.0 / max(prev or t_one, 1e-3) / max(1, args.steps)) + 1))
     if world > 1:
         t_w = torch.tensor([windows], dtype=torch.int64, device="cuda")
         dist.all_reduce(t_w, op=dist.ReduceOp.MAX)
         windows = int(t_w.item())
-    launches0 = venv.launch_count()
-    upd0 = float(venv.stats()[STAT_NAMES.index("pf_updates")])
-    times = []
+    times, launches_timed, upd_sum = [], 0, 0.0
+    i_upd = STAT_NAMES.index("pf_updates")
     with ClockSampler(local) as clocks:
-        for _ in range(windows):
+        for w in range(windows):
+            if w > 0:
+                # every window starts at the episode step the first one did: the
+                # step cost falls as the episode goes on (pings and resamples thin
+                # out), so later windows would not time the same workload
+                venv.reset_all()
+                venv.step_policy("random", args.warmup + settle_steps)
+            upd0 = float(venv.stats()[i_upd])
+            launches0 = venv.launch_count()
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
@@ -459,8 +467,10 @@ def main():
             end.record(stream)
             torch.cuda.synchronize()
             times.append(start.elapsed_time(end))
-    gpu_launches = (venv.launch_count() - launches0) // windows
-    upd_timed = (float(venv.stats()[STAT_NAMES.index("pf_updates")]) - upd0) / windows
+            launches_timed += venv.launch_count() - launches0
+            upd_sum += float(venv.stats()[i_upd]) - upd0
+    gpu_launches = launches_timed // windows
+    upd_timed = upd_sum / windows
     ms = statistics.median(times)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
