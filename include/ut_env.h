@@ -211,8 +211,10 @@ int ut_vecenv_copy_outputs(ut_vecenv* v, const ut_host_outputs* dst);
  * buffers the previous step did not, so the previous step's outputs can be
  * copied out (ut_vecenv_copy_outputs_async) while the next step runs. The
  * pointers of ut_vecenv_buffers() then change with every step (re-query after
- * each); final_obs stays one buffer. Steps and resets wait for an asynchronous
- * copy still reading the set they write. */
+ * each), final_obs included: the step copies the terminal rows the previous
+ * step wrote into the other set, so either set holds every env's latest terminal
+ * observation. Steps and resets wait for an asynchronous copy still reading the
+ * set they write. */
 int ut_vecenv_set_output_buffers(ut_vecenv* v, int n);
 /* Enqueues the D2H copies of the current outputs on `cuda_stream` after the
  * handle's pending work, and returns; synchronize that stream before reading. */

@@ -266,6 +266,8 @@ struct ut_vecenv {
     B.obs = o.obs, B.final_obs = o.final_obs, B.global = o.global, B.rewards = o.rewards, B.track_err = o.track_err;
     B.min_dist = o.min_dist, B.dones = o.dones, B.masks = o.masks, B.lost = o.lost;
     B.collision = o.collision, B.step = o.step;
+    B.prev_final_obs = n_out == 2 ? out[k ^ 1].final_obs : nullptr;
+    B.prev_dones = n_out == 2 ? out[k ^ 1].dones : nullptr;
   }
   // before a kernel writes the output set k
   int wait_outputs(int k) {
@@ -364,9 +366,7 @@ struct ut_vecenv {
     if (n_out == 2) {
       const int t = cur ^ 1;
       if ((rc = wait_outputs(t))) return rc;
-      UT_CUDA(cudaMemcpyAsync(out[t].final_obs, out[cur].final_obs, sizeof(double) * 12 * B.obs_rows,
-                              cudaMemcpyDeviceToDevice, stream));
-      bind_outputs(t);
+      bind_outputs(t);  // the kernel brings set t's final_obs up to date (copy_final_rows)
       cur = t;
       if ((rc = sync_batch())) return rc;
     } else if ((rc = wait_outputs(cur))) {
@@ -757,7 +757,13 @@ int ut_vecenv_set_output_buffers(ut_vecenv* v, int n) {
         (rc = v->alloc(&o.min_dist, (size_t)(E * Tm))) || (rc = v->alloc(&o.lost, (size_t)(E * Tm))) ||
         (rc = v->alloc(&o.collision, (size_t)E)) || (rc = v->alloc(&o.step, (size_t)E)))
       return rc;
-    UT_CUDA(cudaMemsetAsync(o.final_obs, 0, sizeof(double) * 12 * v->B.obs_rows, v->stream));
+    UT_CUDA(cudaMemsetAsync(o.dones, 0, (size_t)E, v->stream));
+  }
+  if (n == 2) {  // both sets start with every terminal row so far (copy_final_rows keeps them so)
+    const ut_vecenv::OutSet &a = v->out[v->cur], &b = v->out[v->cur ^ 1];
+    UT_CUDA(cudaMemcpyAsync(b.final_obs, a.final_obs, sizeof(double) * 12 * v->B.obs_rows, cudaMemcpyDeviceToDevice,
+                            v->stream));
+    UT_CUDA(cudaMemcpyAsync(b.dones, a.dones, (size_t)v->n_envs, cudaMemcpyDeviceToDevice, v->stream));
   }
   if (n == 1 && v->cur == 1) {  // keep the current outputs in set 0
     const ut_vecenv::OutSet &a = v->out[0], &b = v->out[1];
@@ -781,7 +787,8 @@ int ut_vecenv_set_output_buffers(ut_vecenv* v, int n) {
     UT_CUDA(cudaStreamSynchronize(v->stream));
   }
   v->n_out = n;
-  return UT_OK;
+  v->bind_outputs(v->cur);  // the other set's final_obs / dones (or none)
+  return v->sync_batch();
 }
 
 int ut_vecenv_copy_outputs_async(ut_vecenv* v, const ut_host_outputs* d, void* cuda_stream) {

@@ -669,6 +669,22 @@ __device__ __noinline__ void write_outputs(const DevBatch& B, int64_t e0, int64_
   }
 }
 
+// Double-buffered outputs: this step's set last held the outputs of two steps
+// ago; the terminal rows written into the other set at the previous step (its
+// envs with done set) are copied over, so every set holds every env's latest
+// terminal observation (the single buffer's semantics) without a full-buffer copy.
+__device__ __noinline__ void copy_final_rows(const DevBatch& B, int64_t e0, int64_t e1) {
+  const int Am = B.A_max, Rm = B.R_max;
+  const int64_t n = e1 - e0;
+  for (int64_t p = threadIdx.x; p < n * Am * Rm; p += blockDim.x) {
+    const int64_t e = e0 + p / (Am * Rm);
+    if (!B.prev_dones[e]) continue;
+    const int64_t row = e * Am * Rm + (p - (p / (Am * Rm)) * Am * Rm);
+#pragma unroll
+    for (int k = 0; k < 12; ++k) B.final_obs[(int64_t)k * B.obs_rows + row] = B.prev_final_obs[(int64_t)k * B.obs_rows + row];
+  }
+}
+
 // -------------------------------------------------- particle-set phases ---
 template <int PPT>
 struct SetRegs {
@@ -1762,6 +1778,7 @@ __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(De
   for (int e0 = lo; e0 < hi; e0 += blockDim.x) {
     const int e1 = min(hi, e0 + (int)blockDim.x);
     // ---- 3. reward / done / info, one env per thread; then tokens
+    if (B.prev_final_obs) copy_final_rows(Bg, e0, e1);  // ordered before this step's by the barrier below
     {
       const int e = e0 + threadIdx.x;
       if (e < e1) S.flags[threadIdx.x] = env_epilogue(cfg_of(Bg, e), Bg, e) ? kChunkFlagDone : 0;

@@ -100,6 +100,11 @@ struct DevBatch {
   int64_t obs_rows, global_rows;
   double* obs;
   double* final_obs;
+  // double-buffered outputs (ut_vecenv_set_output_buffers(2)): the other set's
+  // final_obs / dones, whose rows of the envs that finished at the previous step
+  // the step copies into this set (null when single-buffered)
+  const double* prev_final_obs;
+  const uint8_t* prev_dones;
   double* global;
   double* rewards;
   uint8_t* dones;

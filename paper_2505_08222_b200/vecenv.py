@@ -220,7 +220,7 @@ class VecEnv:
 
     def _sync_buffers(self):
         _check(self._lib.ut_vecenv_buffers(self._h, C.byref(self._b)))
-        self._views = {k: v for k, v in self._views.items() if k.startswith("pf_") or k == "final_obs"}
+        self._views = {k: v for k, v in self._views.items() if k.startswith("pf_")}
 
     def _after_write(self):
         if self._n_out == 2:

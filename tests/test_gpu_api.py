@@ -170,3 +170,25 @@ def test_multi_step_graph_equals_single_launches(cuda_device):
     for _ in range(3):
         b.step_policy("random", 1)
     assert np.array_equal(a.export_state(), b.export_state())
+
+
+def test_final_obs_rows_persist_across_buffer_sets(cuda_device):
+    """Double-buffered outputs keep the single buffer's final_obs semantics: the
+    terminal rows of an episode stay in final_obs through the following steps
+    of either output set (the step copies the other set's rows of the envs that
+    finished at the previous step), also across a switch from one to two sets."""
+    from paper_2505_08222_b200.vecenv import VecEnv
+    from test_gpu_parity import _to_py
+    cfg = default_config(n_agents=2, n_targets=2, pf_n_particles=64, horizon=3)
+    n = 6
+    ora = Oracle(cfg, n, 31)
+    gpu = VecEnv(_to_py(cfg), n, 31)
+    for s in range(11):
+        if s == 4:
+            gpu.set_output_buffers(2)  # right after the terminal step 3
+        ora.step_policy(1)
+        gpu.step_policy("random", 1)
+        got, want = gpu.host_outputs(["final_obs"])["final_obs"], ora.outputs()["final_obs"]
+        np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12, err_msg=f"step {s}")
+        if s == 8:  # the zero-copy device view of the current set
+            np.testing.assert_allclose(gpu.final_obs_stack().cpu().numpy().T, want, rtol=1e-9, atol=1e-12)
