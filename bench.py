@@ -88,6 +88,53 @@ def oracle_cfg(name, particles=1024):
     return default_config(**kw, pf_n_particles=particles)
 
 
+def make_host_policy(acts_np, n_ag, rank):
+    """The e2e leg's host policy: a uniform legal action per agent from its
+    returned 5-byte mask (the device random policy's rule, vecenv.cpp:125-134).
+    tools/host_policy.c (OpenMP, built by __graft_entry__.build()) when present,
+    else the same rule vectorised in numpy. Padding agents of mixed fleets have no
+    legal action and get 0 (ignored by the step). Returns (fn(masks_u8), name)."""
+    import ctypes as C
+    so = ROOT / "tools" / "_lib" / "libhost_policy.so"
+    if so.exists():
+        lib = C.CDLL(str(so))
+        lib.host_policy.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        lib.host_policy.restype = None
+        counter = C.c_uint64(0)
+        seed = 0x5eed0000 + rank
+        out = acts_np.ctypes.data
+
+        def fn(masks):
+            lib.host_policy(masks.ctypes.data, n_ag, out, seed, C.byref(counter))
+        return fn, "tools/host_policy.c (OpenMP)"
+    import numpy as np
+    rng = np.random.default_rng(rank)
+    kth = np.zeros((32, 5), np.int32)
+    n_legal = np.zeros(32, np.float32)
+    for code in range(32):
+        bits = [b for b in range(5) if (code >> b) & 1]
+        n_legal[code] = len(bits)
+        kth[code, :len(bits)] = bits
+    kth_flat = kth.reshape(-1)
+    u = np.empty(n_ag, np.float32)
+    code = np.empty(n_ag, np.uint8)
+    tmp = np.empty(n_ag, np.uint8)
+    flat = np.empty(n_ag, np.int64)
+
+    def fn(masks):
+        mv = masks.reshape(-1, 5)
+        np.bitwise_or(mv[:, 0], np.left_shift(mv[:, 1], 1, out=tmp), out=code)
+        for b in (2, 3, 4):
+            np.bitwise_or(code, np.left_shift(mv[:, b], b, out=tmp), out=code)
+        rng.random(out=u, dtype=np.float32)
+        np.multiply(u, n_legal.take(code), out=u)
+        flat[:] = u                      # floor (u * #legal) < #legal
+        np.add(flat, code.astype(np.int64) * 5, out=flat)
+        kth_flat.take(flat, out=acts_np)
+    return fn, "numpy (tools/_lib/libhost_policy.so not built)"
+
+
+
 def algorithmic_bytes_per_env_step(A, T, P, rec_words):
     """read + write of the whole state once per step (80 B per
     particle), the env record (read + write), and the step's outputs."""
@@ -546,7 +593,8 @@ def main():
     # The step cost depends on the episode step (pings and resamples thin out as
     # the targets run), so the e2e steps start where the timed window started:
     # a fresh reset, then the same warm-up and settle steps (untimed).
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 10)
+    # the same K steps from the same episode step as the device-timed window
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
     if e2e_steps:
         venv.reset_all()
         venv.step_policy("random", args.warmup + settle_steps)
@@ -575,34 +623,8 @@ def main():
     copy_stream = torch.cuda.Stream()
     rest = {k: v for k, v in host.items() if k != "masks"}
     venv.copy_outputs_into({"masks": host["masks"]})
-    rng = np.random.default_rng(rank)
     acts_np = acts_h.numpy().reshape(-1)
-    # host policy: a uniform legal action per agent from its returned 5-bit mask
-    # (lookup of the j-th set bit, j = floor(u * #legal)), vectorised with
-    # preallocated buffers and 1-D takes; padding agents of mixed fleets have
-    # no legal action and get 0 (ignored by the step)
-    kth = np.zeros((32, 5), np.int32)
-    n_legal = np.zeros(32, np.float32)
-    for code in range(32):
-        bits = [b for b in range(5) if (code >> b) & 1]
-        n_legal[code] = len(bits)
-        kth[code, :len(bits)] = bits
-    kth_flat = kth.reshape(-1)
-    n_ag = n_loc * Am
-    u = np.empty(n_ag, np.float32)
-    code = np.empty(n_ag, np.uint8)
-    tmp = np.empty(n_ag, np.uint8)
-    flat = np.empty(n_ag, np.int64)
-
-    def host_policy(mv):
-        np.bitwise_or(mv[:, 0], np.left_shift(mv[:, 1], 1, out=tmp), out=code)
-        for b in (2, 3, 4):
-            np.bitwise_or(code, np.left_shift(mv[:, b], b, out=tmp), out=code)
-        rng.random(out=u, dtype=np.float32)
-        np.multiply(u, n_legal.take(code), out=u)
-        flat[:] = u                      # floor (u * #legal) < #legal
-        np.add(flat, code.astype(np.int64) * 5, out=flat)
-        kth_flat.take(flat, out=acts_np)
+    host_policy, policy_impl = make_host_policy(acts_np, n_loc * Am, rank)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -610,7 +632,7 @@ def main():
     split = {"host_policy": 0.0, "step_call": 0.0, "masks_d2h": 0.0, "async_enqueue": 0.0}
     for _ in range(e2e_steps):
         ta = time.perf_counter()
-        host_policy(host["masks"].numpy().reshape(-1, 5))
+        host_policy(host["masks"].numpy())
         tb = time.perf_counter()
         venv.step(acts_h)
         tc = time.perf_counter()
@@ -657,11 +679,11 @@ def main():
                        window_ms=[round(x, 4) for x in times]),
         "e2e": {"value": e2e_value, "unit": "agent-env steps/s", "h2d_bytes_per_step": h2d,
                 "ms_per_step_split": {k: 1e3 * v / max(1, e2e_steps) for k, v in split.items()},
-                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "host_policy": policy_impl,
                 "path": "VecEnv.step(host int32 actions from a host policy on the returned masks) + every output "
                         "to pinned host (ut_vecenv_step, ut_vecenv_copy_outputs for the masks, "
                         "ut_vecenv_copy_outputs_async for the rest, overlapping the next step); the e2e "
-                        "steps start at the episode step the timed window starts at (reset + the same "
+                        "steps are the timed window's K steps from the same episode step (reset + the same "
                         "warm-up and settle steps), on the handle's own stream"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,

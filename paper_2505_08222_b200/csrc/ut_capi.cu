@@ -672,7 +672,7 @@ namespace {
 // First half of VecEnv::step (vecenv.cpp:79-93): stage the actions and validate
 // every env's actions on the device; nothing is mutated. The result is read by
 // validate_result() once the stream has reached it.
-int enqueue_validate(ut_vecenv* v, const int32_t* actions, int actions_on_device) {
+int enqueue_validate(ut_vecenv* v, const int32_t* actions, int actions_on_device, bool with_status = true) {
   const size_t n = (size_t)(v->n_envs * v->A_max);
   UT_CUDA(cudaMemcpyAsync(const_cast<int32_t*>(v->B.actions), actions, n * sizeof(int32_t),
                           actions_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, v->stream));
@@ -682,16 +682,13 @@ int enqueue_validate(ut_vecenv* v, const int32_t* actions, int actions_on_device
   validate_kernel<<<(unsigned)((v->n_envs + tpb - 1) / tpb), tpb, 0, v->stream>>>(v->B);
   ++v->launches;
   UT_CUDA(cudaGetLastError());
-  return v->enqueue_status();
+  return with_status ? v->enqueue_status() : UT_OK;
 }
 
 // UT_ERR_CONTRACT for the lowest env whose action failed validation, its index
 // shown as `shown_base + e` (the global index for a shard of a multi-device
 // handle); message format of env.cpp:241-246 prefixed like vecenv.cpp:88-93.
-int validate_result(ut_vecenv* v, int64_t shown_base) {
-  UT_CUDA(cudaStreamSynchronize(v->stream));
-  if (v->h_status[1] == INT_MAX) return UT_OK;
-  const int64_t e = v->h_status[1];
+int validate_error(ut_vecenv* v, int64_t e, int64_t shown_base) {
   const long long shown = (long long)(shown_base + e);
   std::vector<int32_t> acts((size_t)v->A_max);
   UT_CUDA(cudaMemcpy(acts.data(), v->B.actions + e * v->A_max, sizeof(int32_t) * v->A_max, cudaMemcpyDeviceToHost));
@@ -707,14 +704,34 @@ int validate_result(ut_vecenv* v, int64_t shown_base) {
   }
   return fail(UT_ERR_CONTRACT, "env %lld: step: invalid action", shown);
 }
+int validate_result(ut_vecenv* v, int64_t shown_base) {
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  if (v->h_status[1] == INT_MAX) return UT_OK;
+  return validate_error(v, v->h_status[1], shown_base);
+}
 }  // namespace
 
 int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device) {
   DeviceGuard dg(v->device);
+  // The step kernel itself is gated on the validation result (it returns before
+  // touching anything when an action failed), so validation and step go out
+  // together and the host waits once: no round trip between them, whose status
+  // copy would also queue behind a caller's asynchronous output copies still
+  // draining from the previous step.
   int rc;
-  if ((rc = enqueue_validate(v, actions, actions_on_device)) || (rc = validate_result(v, 0))) return rc;
-  if ((rc = v->launch_step(MODE_EXTERNAL))) return rc;
-  return v->check_status("step");
+  if ((rc = enqueue_validate(v, actions, actions_on_device, false))) return rc;
+  const int prev_cur = v->cur;
+  if ((rc = v->launch_step(MODE_EXTERNAL)) || (rc = v->enqueue_status())) return rc;
+  UT_CUDA(cudaStreamSynchronize(v->stream));
+  if (v->h_status[1] != INT_MAX) {  // nothing moved: undo the output-set switch
+    if (v->cur != prev_cur) {
+      v->cur = prev_cur;
+      v->bind_outputs(prev_cur);
+      if ((rc = v->sync_batch())) return rc;
+    }
+    return validate_error(v, v->h_status[1], 0);
+  }
+  return v->finish_status("step");
 }
 
 int ut_vecenv_step_policy(ut_vecenv* v, int policy, int n_steps) {

@@ -1675,6 +1675,9 @@ __device__ __forceinline__ void reinit_chunk(const DevBatch& B, int64_t e0, int6
 // The fused step.
 template <int PPT, int NP, bool FULL>
 __global__ void __launch_bounds__(1024 / PPT, UT_STEP_MIN_BLOCKS) step_kernel(DevBatch B, int mode, int32_t* status) {
+  // external actions: nothing moves unless every action passed validate_kernel
+  // (launched just before on the same stream; vecenv.cpp:88-93 validates all first)
+  if (mode == MODE_EXTERNAL && *B.error_env != INT_MAX) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const Smem S = carve<NP>(smem_raw, B.cfgs[0].sA, B.cfgs[0].sT);
   const DevBatch& Bg = *B.self;  // cold paths read the global copy

@@ -192,3 +192,33 @@ def test_final_obs_rows_persist_across_buffer_sets(cuda_device):
         np.testing.assert_allclose(got, want, rtol=1e-9, atol=1e-12, err_msg=f"step {s}")
         if s == 8:  # the zero-copy device view of the current set
             np.testing.assert_allclose(gpu.final_obs_stack().cpu().numpy().T, want, rtol=1e-9, atol=1e-12)
+
+
+def test_invalid_action_with_double_buffered_outputs_moves_nothing(cuda_device):
+    """The step kernel is gated on the validation result on the device (one host
+    wait per step): an invalid action leaves the state, the current output set and
+    the next valid step exactly as if the bad call had never been made, also with
+    two output sets (the switch to the other set is undone)."""
+    from paper_2505_08222_b200.vecenv import ContractViolation, VecEnv
+    cfg = _to_py(default_config(n_agents=2, n_targets=2, pf_n_particles=1024, horizon=5))
+    a, b = VecEnv(cfg, 6, 11), VecEnv(cfg, 6, 11)
+    a.set_output_buffers(2)
+    b.set_output_buffers(2)
+    rng = np.random.default_rng(3)
+    for s in range(7):  # crosses an auto-reset
+        acts = random_legal_actions(a.host_outputs(["masks"])["masks"], rng).reshape(6, 2)
+        if s in (2, 5):
+            bad = acts.copy()
+            bad[4, 1] = 7
+            before = a.export_state()
+            out_before = a.host_outputs()
+            with pytest.raises(ContractViolation, match=r"^env 4: step: invalid action 7 for agent 1"):
+                a.step(bad)
+            assert np.array_equal(before, a.export_state())
+            out_after = a.host_outputs()
+            assert all(np.array_equal(out_before[k], out_after[k]) for k in out_before)
+        a.step(acts)
+        b.step(acts)
+        assert np.array_equal(a.export_state(), b.export_state())
+        ha, hb = a.host_outputs(), b.host_outputs()
+        assert all(np.array_equal(ha[k], hb[k]) for k in ha)
