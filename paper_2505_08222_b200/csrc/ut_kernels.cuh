@@ -1161,16 +1161,29 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     }
   }
   const double ms = tk[TK_MAXSPEED];
-  // branch-free (no clamp when ms <= 0, tracking.cpp:105): the quotient is
-  // formed for every particle (sp = 0 or ms <= 0 give values the select drops)
-  const bool clamp_on = ms > 0.0;
+  // No clamp when ms <= 0 (tracking.cpp:105). A speed^2 at or below lo < ms^2
+  // (exactly: RN(ms^2) (1 - 2^-50) rounded stays below it) has RN(sqrt) <= ms,
+  // so f = 1 and the particle is unchanged: warps with no particle above lo
+  // skip the correctly rounded sqrt and division (about half of them: the fast
+  // particles cluster after resampling). Otherwise branch-free per particle (sp
+  // = 0 gives a quotient the select drops).
+  const double lo = (ms * ms) * (1.0 - 0x1p-50);
+  double v2[PPT];
+  bool over = false;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
-    const double sp = sqrt_rn_clamp(s.vx[j] * s.vx[j] + s.vy[j] * s.vy[j]);
-    const double qt = div_rn_clamp(ms, sp);
-    const double f = clamp_on && sp > ms ? qt : 1.0;
-    s.vx[j] = s.vx[j] * f;
-    s.vy[j] = s.vy[j] * f;
+    v2[j] = s.vx[j] * s.vx[j] + s.vy[j] * s.vy[j];
+    over |= v2[j] > lo;
+  }
+  if (ms > 0.0 && __any_sync(0xffffffffu, over)) {
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+      const double sp = sqrt_rn_clamp(v2[j]);
+      const double qt = div_rn_clamp(ms, sp);
+      const double f = sp > ms ? qt : 1.0;
+      s.vx[j] = s.vx[j] * f;
+      s.vy[j] = s.vy[j] * f;
+    }
   }
   ph_mark(B, PH_FILTER);
 
