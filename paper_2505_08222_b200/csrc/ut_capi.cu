@@ -1327,8 +1327,9 @@ __global__ void cr_grid_kernel(int q, float* out) {
 // The production (table-driven) path: the same functions box_muller_fast is
 // built from, falling back exactly like the step kernel does.
 __global__ void cr_grid_fast_kernel(int q, float* out) {
-  __shared__ double2 tl[128], ts[64 * 8];
-  for (int i = threadIdx.x; i < 128; i += blockDim.x) tl[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
+  __shared__ double2 tl[128 * 8], ts[64 * 8];
+  for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x)
+    tl[i] = make_double2(kLogTab[2 * (i >> 3)], kLogTab[2 * (i >> 3) + 1]);
   for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x)
     ts[i] = make_double2(kSinCosTab[2 * (i >> 3)], kSinCosTab[2 * (i >> 3) + 1]);
   __syncthreads();
@@ -1361,7 +1362,7 @@ __global__ void ieee_check_kernel(int kind, uint64_t seed, int64_t n, unsigned l
       // libm exp over [-760, 0]: results more than 1 ulp off
       const double* tab = kExp2Tab;
       const double x = -760.0 * u;
-      const long long a = __double_as_longlong(exp_neg(x, tab)), b = __double_as_longlong(exp(x));
+      const long long a = __double_as_longlong(exp_neg<1>(x, tab)), b = __double_as_longlong(exp(x));
       local += (a - b > 1 || b - a > 1);
     } else if (kind == 2 || kind == 3) {
       // the likelihood distance sqrt (sqrt_dist) against IEEE over squared

@@ -33,6 +33,8 @@ namespace cg = cooperative_groups;
 enum StepMode : int { MODE_EXTERNAL = -1, MODE_RANDOM = 0, MODE_SCRIPTED = 1 };
 enum DevStatus : int { ST_OK = 0, ST_SPAWN_INFEASIBLE = 2 };
 constexpr int kMaxMerged = 8;     // merged update handles up to 8 measurements per set
+constexpr int kMbStride = 36;     // stage-maxima row stride (uint32; 8 x 36 fit one reducer buffer)
+static_assert(kMaxMerged * kMbStride <= 2 * kRedSlots, "stage maxima exceed a reducer buffer");
 constexpr int kMeasStride = 8;    // ox, oy, r2, sigma, -1/(2 sigma^2) (+pad)
 constexpr int kMaxEntities = 64;  // spawn scratch per thread
 constexpr double kMergeFloor = 0x1p-860;  // see the merged-update argument in step_set
@@ -59,9 +61,9 @@ __device__ __forceinline__ Rec rec_of(const DevBatch& B, int64_t e) { return Rec
 enum : int { TK_POS = 0, TK_MAXSPEED, TK_EX, TK_EY, TK_ESSOK, TK_AGE, TK_EVER, TK_KEY, kTrkStride };
 
 struct Smem {
-  double2* tab_log;  // [128]
+  double2* tab_log;  // [128][8] (replicated, see log_table)
   double2* tab_sc;   // [64][8] (replicated, see sincos_table)
-  double* tab_exp;   // [32]
+  double* tab_exp;   // [32][16] (replicated, see exp_neg)
   DevConfig* cfg;    // config of the env being filtered
   double* red;       // kRedDoubles: BlockReducer buffers + scan warp sums
   double* bc;        // 16 broadcast slots (0: resample draw; kBcStat*: the env's filter statistics)
@@ -76,6 +78,7 @@ struct Smem {
   double* pf;        // [5][P] TMA-prefetched next particle set
   double* cum;       // [P] resample scan | re-init words
   double* st;        // [4P] resample staging
+  double2* park;     // [2][P/2] vx, vy of the merged pass, pair-chunked (park_field)
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -86,9 +89,9 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 // fleet-sized regions follow at runtime offsets.
 template <int NP>
 struct FixedSmem {
-  double2 tab_log[128];
+  double2 tab_log[128 * 8];
   double2 tab_sc[64 * 8];
-  double tab_exp[32];
+  double tab_exp[32 * 16];
   double red[kRedDoubles];
   double bc[16];
   uint64_t mbar[2];
@@ -102,6 +105,10 @@ struct FixedSmem {
   // every thread holds its particles) the staging of the exact update and the
   // resample, and in the reset phase the re-init words
   double pf[5 * NP];
+  // vx / vy parked during the merged pass's likelihood stages, in lane-contiguous
+  // 16-byte chunks (the set buffer's own-slot layout puts a quarter-warp's 128-bit
+  // accesses on half the banks)
+  double2 park[NP];
   DevConfig cfg;
 };
 
@@ -138,6 +145,7 @@ __device__ __forceinline__ Smem carve(unsigned char* base, int sA, int sT) {
   S.pf = F.pf;
   S.st = F.pf;
   S.cum = F.pf + 4 * NP;
+  S.park = F.park;
   size_t o = align16(sizeof(FixedSmem<NP>));
   S.meas = (double*)(base + o);
   o += align16(sizeof(double) * kMeasStride * sA * sT);
@@ -201,10 +209,11 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 
 __device__ __forceinline__ void load_tables(const Smem& S) {
-  for (int i = threadIdx.x; i < 128; i += blockDim.x) S.tab_log[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
+  for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x)
+    S.tab_log[i] = make_double2(kLogTab[2 * (i >> 3)], kLogTab[2 * (i >> 3) + 1]);
   for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x)
     S.tab_sc[i] = make_double2(kSinCosTab[2 * (i >> 3)], kSinCosTab[2 * (i >> 3) + 1]);
-  for (int i = threadIdx.x; i < 32; i += blockDim.x) S.tab_exp[i] = kExp2Tab[i];
+  for (int i = threadIdx.x; i < 32 * 16; i += blockDim.x) S.tab_exp[i] = kExp2Tab[i >> 4];
 }
 
 // The CTA's contiguous env range.
@@ -953,6 +962,23 @@ __device__ __forceinline__ void load_field(const double* f, int k0, double (&v)[
   }
 }
 
+// One field of this thread's PPT particles to / from a parking area of pair
+// chunks: particles (k0 + q, k0 + q + 1) at chunk (q / 2) NT + tid, so a warp's
+// 128-bit accesses are contiguous (conflict-free).
+template <int PPT>
+__device__ __forceinline__ void park_field(double2* f, int nt, const double (&v)[PPT]) {
+#pragma unroll
+  for (int q = 0; q < PPT; q += 2) f[(q / 2) * nt + threadIdx.x] = make_double2(v[q], v[q + 1]);
+}
+template <int PPT>
+__device__ __forceinline__ void unpark_field(const double2* f, int nt, double (&v)[PPT]) {
+#pragma unroll
+  for (int q = 0; q < PPT; q += 2) {
+    const double2 t = f[(q / 2) * nt + threadIdx.x];
+    v[q] = t.x, v[q + 1] = t.y;
+  }
+}
+
 // Per-phase cycle profile of the particle-set loop (debug builds with
 // -DUT_SET_PROFILE only; thread 0 of each CTA, read by ut_debug_set_profile).
 constexpr int kSetProfSlots = 12;
@@ -1130,6 +1156,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // after which the staging may start)
   const bool merged = nm > 0 && !exact;
   const int NPf = (int)(S.cum - S.pf) / 4;  // field stride of the set buffer
+  const int NT = NW > 0 ? NW * 32 : (int)blockDim.x;
   if (FULL) {
     SETPROF(0);
     mbar_wait_sa(S.mbar_sa, tphase);
@@ -1193,8 +1220,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   bool have_ess = false;
   double ess = 0.0;
   if (merged) {
-    store_field<PPT>(S.pf + 2 * NPf, k0, s.vx);
-    store_field<PPT>(S.pf + 3 * NPf, k0, s.vy);
+    park_field<PPT>(S.park, NT, s.vx);
+    park_field<PPT>(S.park + NT * (PPT / 2), NT, s.vy);
     if (!FULL) store_field<PPT>(S.pf + 4 * NPf, k0, s.w);
   }
   if (nm > 0 && !exact) {
@@ -1212,7 +1239,9 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     double L[PPT];
 #pragma unroll
     for (int q = 0; q < PPT; ++q) L[q] = 0.0;
-    float* mb = reinterpret_cast<float*>(R.buf());  // per-stage warp maxima, [stage * 32 + warp]
+    // per-stage warp maxima, [stage * kMbStride + warp]: the stride keeps the
+    // stage lanes' 128-bit reads below on distinct banks
+    float* mb = reinterpret_cast<float*>(R.buf());
     // one stage: every particle's log-likelihood for measurement j, added to L in
     // stage order, and the stage's warp maximum (rounded up to fp32)
     // Every ll is <= 0, so its high word, read as unsigned, grows with |ll|: the
@@ -1238,7 +1267,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     };
     auto stage_max = [&](int j, uint32_t mj) {
       mj = redux_min_u32(mj);
-      st_shared_if(lane == 0, reinterpret_cast<uint32_t*>(mb) + j * 32 + warp, mj);
+      st_shared_if(lane == 0, reinterpret_cast<uint32_t*>(mb) + j * kMbStride + warp, mj);
     };
     // two stages per iteration so their distance / sqrt chains interleave (the
     // warp reductions, whose divergence check fences the scheduler, follow both)
@@ -1262,11 +1291,11 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       if constexpr (NW > 0 && NW % 4 == 0) {
 #pragma unroll
         for (int v = 0; v < NW; v += 4) {
-          const uint4 m4 = *reinterpret_cast<const uint4*>(mbu + lane * 32 + v);
+          const uint4 m4 = *reinterpret_cast<const uint4*>(mbu + lane * kMbStride + v);
           hl = min(hl, min(min(m4.x, m4.y), min(m4.z, m4.w)));
         }
       } else {
-        for (int v = 0; v < nw; ++v) hl = min(hl, mbu[lane * 32 + v]);
+        for (int v = 0; v < nw; ++v) hl = min(hl, mbu[lane * kMbStride + v]);
       }
     }
     // the sum over lanes 0..7 (nm <= kMaxMerged = 8) by an xor butterfly (every
@@ -1282,8 +1311,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     if (!isfinite(shift)) {
       exact = true;
       if (merged) {  // before the exact path's staging barrier
-        load_field<PPT>(S.pf + 2 * NPf, k0, s.vx);
-        load_field<PPT>(S.pf + 3 * NPf, k0, s.vy);
+        unpark_field<PPT>(S.park, NT, s.vx);
+        unpark_field<PPT>(S.park + NT * (PPT / 2), NT, s.vy);
       }
     } else {
       double e[PPT], ls = 0.0, lq = 0.0;
@@ -1297,8 +1326,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         }
       }
       if (merged) {  // before the barrier after which the staging may start
-        load_field<PPT>(S.pf + 2 * NPf, k0, s.vx);
-        load_field<PPT>(S.pf + 3 * NPf, k0, s.vy);
+        unpark_field<PPT>(S.park, NT, s.vx);
+        unpark_field<PPT>(S.park + NT * (PPT / 2), NT, s.vy);
       }
       SETPROF(4);
       // the guards on max(e) from the sum: sum >= 2^-850 gives max >= sum / P >=
