@@ -193,7 +193,9 @@ void ut_vecenv_destroy(ut_vecenv* v);
 int ut_vecenv_reset_all(ut_vecenv* v);
 /* VecEnv::step (vecenv.cpp:79-116): actions row-major n_envs x n_agents, host or
  * device memory. Every action is validated BEFORE any env steps; on a violation
- * nothing is mutated and UT_ERR_CONTRACT names the lowest failing env ("env i: ..."). */
+ * nothing is mutated and UT_ERR_CONTRACT names the lowest failing env ("env i: ...").
+ * Validation and step are enqueued together (the step kernel is gated on the
+ * validation result on the device) and the call returns after ONE wait. */
 int ut_vecenv_step(ut_vecenv* v, const int32_t* actions, int actions_on_device);
 /* VecEnv::step_policy (vecenv.cpp:118-143), policy UT_POLICY_*. n_steps > 1 runs
  * that many steps back to back with no host round trip in between, as ONE CUDA

@@ -13,6 +13,7 @@ O=gpurun_out
 mkdir -p $O
 nvidia-smi -q -d CLOCK > $O/${TAG}_clocks_before.txt 2>&1
 timeout 600 python bench.py > $O/${TAG}_bench_c3.json 2> $O/${TAG}_bench_c3.err
+timeout 600 python bench.py --impl reference > $O/${TAG}_bench_reference_arm.json 2> $O/${TAG}_bench_reference_arm.err
 for c in c1 c2 c4 c5; do
   timeout 600 python bench.py --config $c --no-cpu-baseline > $O/${TAG}_bench_$c.json 2> $O/${TAG}_bench_$c.err
 done
