@@ -1327,9 +1327,8 @@ __global__ void cr_grid_kernel(int q, float* out) {
 // The production (table-driven) path: the same functions box_muller_fast is
 // built from, falling back exactly like the step kernel does.
 __global__ void cr_grid_fast_kernel(int q, float* out) {
-  __shared__ double2 tl[128 * 8], ts[64 * 8];
-  for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x)
-    tl[i] = make_double2(kLogTab[2 * (i >> 3)], kLogTab[2 * (i >> 3) + 1]);
+  __shared__ double2 tl[128], ts[64 * 8];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) tl[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
   for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x)
     ts[i] = make_double2(kSinCosTab[2 * (i >> 3)], kSinCosTab[2 * (i >> 3) + 1]);
   __syncthreads();

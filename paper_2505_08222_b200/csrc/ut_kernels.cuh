@@ -61,7 +61,7 @@ __device__ __forceinline__ Rec rec_of(const DevBatch& B, int64_t e) { return Rec
 enum : int { TK_POS = 0, TK_MAXSPEED, TK_EX, TK_EY, TK_ESSOK, TK_AGE, TK_EVER, TK_KEY, kTrkStride };
 
 struct Smem {
-  double2* tab_log;  // [128][8] (replicated, see log_table)
+  double2* tab_log;  // [128]
   double2* tab_sc;   // [64][8] (replicated, see sincos_table)
   double* tab_exp;   // [32][16] (replicated, see exp_neg)
   DevConfig* cfg;    // config of the env being filtered
@@ -89,7 +89,7 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(
 // fleet-sized regions follow at runtime offsets.
 template <int NP>
 struct FixedSmem {
-  double2 tab_log[128 * 8];
+  double2 tab_log[128];
   double2 tab_sc[64 * 8];
   double tab_exp[32 * 16];
   double red[kRedDoubles];
@@ -209,8 +209,7 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 }
 
 __device__ __forceinline__ void load_tables(const Smem& S) {
-  for (int i = threadIdx.x; i < 128 * 8; i += blockDim.x)
-    S.tab_log[i] = make_double2(kLogTab[2 * (i >> 3)], kLogTab[2 * (i >> 3) + 1]);
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) S.tab_log[i] = make_double2(kLogTab[2 * i], kLogTab[2 * i + 1]);
   for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x)
     S.tab_sc[i] = make_double2(kSinCosTab[2 * (i >> 3)], kSinCosTab[2 * (i >> 3) + 1]);
   for (int i = threadIdx.x; i < 32 * 16; i += blockDim.x) S.tab_exp[i] = kExp2Tab[i >> 4];
