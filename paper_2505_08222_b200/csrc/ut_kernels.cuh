@@ -778,7 +778,9 @@ __device__ __noinline__ int pf_update_seq(const double* m, int k0, int P, const 
 template <int PPT, bool FULL, int NW>
 __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, int P, double cx, double cy,
                                                BlockReducer& R, bool uniform = false, double inv_n = 0.0) {
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  // -0.0 is the exact identity of IEEE addition, so the first term's add folds
+  // away (0.0 + x is not an identity: x = -0.0)
+  double a0 = -0.0, a1 = -0.0, a2 = -0.0;
   if (uniform) {  // weights all 1/n (just resampled): plain moments, scaled once
 #pragma unroll
     for (int j = 0; j < PPT; ++j) {
@@ -862,7 +864,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
     for (int i = 0; i < PPT; i += 4) *reinterpret_cast<int4*>(mark + k0 + i) = make_int4(0, 0, 0, 0);
   }
   ut_bar();
-  double woff = 0.0;  // cum[k] = (sum of earlier warps' totals + excl) + loc[q]
+  double woff = -0.0;  // cum[k] = (sum of earlier warps' totals + excl) + loc[q]; -0.0: see pf_estimate
   if constexpr (NW > 0) {
 #pragma unroll
     for (int v = 0; v < NW - 1; ++v)
@@ -1314,7 +1316,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         unpark_field<PPT>(S.park + NT * (PPT / 2), NT, s.vy);
       }
     } else {
-      double e[PPT], ls = 0.0, lq = 0.0;
+      double e[PPT], ls = -0.0, lq = -0.0;  // -0.0: see pf_estimate
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         e[q] = 0.0;
