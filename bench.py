@@ -98,15 +98,18 @@ def make_host_policy(acts_np, n_ag, rank):
     so = ROOT / "tools" / "_lib" / "libhost_policy.so"
     if so.exists():
         lib = C.CDLL(str(so))
-        lib.host_policy.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64)]
+        lib.host_policy.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.c_int]
         lib.host_policy.restype = None
         counter = C.c_uint64(0)
         seed = 0x5eed0000 + rank
         out = acts_np.ctypes.data
+        # the node's cores split over the ranks on it
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", os.environ.get("WORLD_SIZE", "1")))
+        n_threads = max(1, (os.cpu_count() or 1) // max(1, local_world))
 
         def fn(masks):
-            lib.host_policy(masks.ctypes.data, n_ag, out, seed, C.byref(counter))
-        return fn, "tools/host_policy.c (OpenMP)"
+            lib.host_policy(masks.ctypes.data, n_ag, out, seed, C.byref(counter), n_threads)
+        return fn, f"tools/host_policy.c (OpenMP, {n_threads} threads)"
     import numpy as np
     rng = np.random.default_rng(rank)
     kth = np.zeros((32, 5), np.int32)

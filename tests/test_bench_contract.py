@@ -56,3 +56,33 @@ def test_gpus_flag_spawns_one_rank_per_gpu(cfg, gpus, scaling, total):
     assert d["envs_sum"] == total and d["max_rank"] == gpus and d["backend"] == "gloo"
     r = d["ranges"]
     assert r[0][0] == 0 and r[-1][1] == total and all(a[1] == b[0] for a, b in zip(r, r[1:]))
+
+
+@pytest.mark.parametrize("native", [True, False])
+def test_e2e_host_policy_draws_legal_actions(native, monkeypatch):
+    """The e2e leg's host policy (tools/host_policy.c, or its numpy twin): a legal
+    action for every agent with one, 0 for agents without, about uniform over the
+    legal ones, and a fresh draw every call."""
+    import numpy as np
+    n = 20000
+    if not native:
+        monkeypatch.setattr(bench, "ROOT", ROOT / "no-such-dir")
+    elif not (ROOT / "tools" / "_lib" / "libhost_policy.so").exists():
+        pytest.skip("tools/_lib/libhost_policy.so not built")
+    acts = np.zeros(n, np.int32)
+    fn, name = bench.make_host_policy(acts, n, 0)
+    assert ("host_policy.c" in name) == native
+    rng = np.random.default_rng(1)
+    masks = (rng.random((n, 5)) < 0.6).astype(np.uint8)
+    masks[:100] = 0  # no legal action (padding agents of a mixed fleet)
+    fn(masks.reshape(-1))
+    first = acts.copy()
+    none = masks.sum(axis=1) == 0
+    assert np.all(first[none] == 0)
+    assert (masks[np.arange(n), first] == 1)[~none].all()
+    only2 = np.flatnonzero((masks == [0, 0, 1, 0, 0]).all(axis=1))
+    assert np.all(first[only2] == 2)
+    both = np.flatnonzero((masks == [1, 1, 0, 0, 0]).all(axis=1))
+    assert 0.35 < np.mean(first[both] == 1) < 0.65
+    fn(masks.reshape(-1))
+    assert not np.array_equal(first, acts)

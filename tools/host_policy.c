@@ -16,7 +16,8 @@ static inline uint64_t splitmix64(uint64_t x) {
 }
 
 /* masks: n_agents x 5 bytes (0/1); actions: n_agents int32; *counter advances
- * by n_agents per call (the stream position). */
+ * by n_agents per call (the stream position); n_threads: the host threads this
+ * rank may use (the node's cores split over its ranks). */
 static int32_t kth[32][5];
 static int kth_ready = 0;
 
@@ -29,10 +30,11 @@ static void kth_init(void) {
   kth_ready = 1;
 }
 
-void host_policy(const uint8_t* masks, int64_t n_agents, int32_t* actions, uint64_t seed, uint64_t* counter) {
+void host_policy(const uint8_t* masks, int64_t n_agents, int32_t* actions, uint64_t seed, uint64_t* counter,
+                 int n_threads) {
   const uint64_t base = *counter;
   if (!kth_ready) kth_init();
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) num_threads(n_threads)
   for (int64_t i = 0; i < n_agents; ++i) {
     const uint8_t* m = masks + 5 * i;
     const unsigned code = (unsigned)m[0] | (unsigned)m[1] << 1 | (unsigned)m[2] << 2 | (unsigned)m[3] << 3 |
