@@ -821,76 +821,68 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
   return make_double3(mx, my, sqrt_rn_clamp(R.sum<NW>(acc)));  // >= 0: 0 or far above 2^-960
 }
 
-// pf::resample (tracking.cpp:147-170): inclusive scan of w in index order, then
-// output j takes the first particle whose cumulative weight reaches (j + u0)/n,
-// clamped to n - 1 (the reference's monotone two-pointer walk).
+// Stage this thread's particles for the resample gather: particle k = k0 + q of
+// thread t at q * NT + t, so each field's stores are lane-contiguous
+// (conflict-free); positions and velocities as pairs, one 128-bit access each.
 template <int PPT, bool FULL, int NW>
-__device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double inv_n, const Smem& S) {
+__device__ __forceinline__ void resample_stage(const SetRegs<PPT>& s, int k0, int P, const Smem& S) {
   const int tid = threadIdx.x;
-  int* mark = reinterpret_cast<int*>(S.cum);  // [P] source marks of the outputs
-  double* st = S.st;
-  double* wsum = S.red + 2 * kRedSlots;  // [32] warp totals, then [32] int warp maxima at +96
-  // Staging layout: particle k = k0 + q of thread t at q * NT + t, so each
-  // field's stores are lane-contiguous (conflict-free); a field spans FS slots.
-  // Positions and velocities are staged as pairs, one 128-bit access each.
   const int NT = NW > 0 ? NW * 32 : (int)blockDim.x;
   const int FS = NT * PPT;
-  double2* st2 = reinterpret_cast<double2*>(st);  // [FS] (px, py), then [FS] (vx, vy)
-  double loc[PPT];
-  double run = 0.0;
+  double2* st2 = reinterpret_cast<double2*>(S.st);  // [FS] (px, py), then [FS] (vx, vy)
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
-    const int k = k0 + q;
-    if (FULL || k < P) {
+    if (FULL || k0 + q < P) {
       st2[q * NT + tid] = make_double2(s.px[q], s.py[q]);
       st2[FS + q * NT + tid] = make_double2(s.vx[q], s.vy[q]);
-      run = q == 0 ? s.w[q] : run + s.w[q];
     }
-    loc[q] = run;
   }
-  const int lane = tid & 31, warp = tid >> 5;
-  double incl = run;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl = incl + y;
-  }
-  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
-  if (lane == 0) excl = 0.0;
-  st_shared_if(lane == 31, wsum + warp, incl);
+}
+
+// Zero this thread's resample marks (S.cum as int[P]; before a barrier that
+// precedes the marking, and after every thread's last read of the set buffer's
+// w field, which the marks alias).
+template <int PPT, bool FULL>
+__device__ __forceinline__ void resample_zero_marks(int k0, int P, const Smem& S) {
   static_assert(PPT % 4 == 0, "mark zeroing takes whole int4s");
+  int* mark = reinterpret_cast<int*>(S.cum);
   if (FULL || k0 < P) {
 #pragma unroll
     for (int i = 0; i < PPT; i += 4) *reinterpret_cast<int4*>(mark + k0 + i) = make_int4(0, 0, 0, 0);
   }
-  ut_bar();
-  double woff = -0.0;  // cum[k] = (sum of earlier warps' totals + excl) + loc[q]; -0.0: see pf_estimate
-  if constexpr (NW > 0) {
-#pragma unroll
-    for (int v = 0; v < NW - 1; ++v)
-      if (v < warp) woff = woff + wsum[v];
-  } else {
-    for (int v = 0; v < warp; ++v) woff = woff + wsum[v];
-  }
-  const double base = woff + excl;
-  // Output j takes the first particle i with cum[i] >= u_j, u_j = (j + u0)/n
-  // (clamped to n - 1). With count(c) = #{j : u_j <= c}, the outputs
-  // [count(cum[i-1]), count(cum[i])) are particle i's: particle k marks
-  // count(cum[k]) with k + 1 (the max wins where zero-weight particles share a
-  // boundary) and a prefix max over the marks (0 where unmarked) hands every
-  // output its source; outputs past count(cum[n-2]) fall to n - 1.
-  // count(c) = floor(c n - u0) + 1, clamped to [0, n]. It can differ from the
-  // count against the rounded u_j = (j + u0)/n only when c n - u0 lies within
-  // ~1e-13 of an integer; the block-tree cumulative weights already differ
-  // from the reference's sequential ones by ~1e-15 (x n = 1e-12), so exact
-  // boundary tests would not make a flip any less likely.
-  // As (base + loc) n + (1 - u0) >= 0, truncation gives the +1 and the clamp at
-  // 0 for free: count = min(n, trunc(loc n + (base n + 1 - u0))).
-  const double c0 = fma(base, (double)P, 1.0 - u0);
+}
+
+// The selection half of pf::resample (tracking.cpp:147-170), once the marks are
+// zeroed and the particles staged (both ordered by a barrier before the marks
+// are set). Particle k = k0 + q has cumulative weight times n equal to
+// loc[q] * scale + c0 - (1 - u0); output j takes the first particle whose
+// cumulative weight reaches (j + u0)/n, clamped to n - 1 (the reference's
+// monotone two-pointer walk).
+// With count(c) = #{j : u_j <= c}, the outputs [count(cum[i-1]), count(cum[i]))
+// are particle i's: particle k marks count(cum[k]) with k + 1 (the max wins
+// where zero-weight particles share a boundary) and a prefix max over the marks
+// (0 where unmarked) hands every output its source; outputs past
+// count(cum[n-2]) fall to n - 1.
+// count(c) = floor(c n - u0) + 1, clamped to [0, n]. It can differ from the
+// count against the rounded u_j = (j + u0)/n only when c n - u0 lies within
+// ~1e-13 of an integer; the block-tree cumulative weights already differ
+// from the reference's sequential ones by ~1e-15 (x n = 1e-12), so exact
+// boundary tests would not make a flip any less likely.
+// As cum n + (1 - u0) >= 0, truncation gives the +1 and the clamp at 0 for
+// free: count = min(n, trunc(loc scale + c0)).
+template <int PPT, bool FULL, int NW>
+__device__ void resample_select(SetRegs<PPT>& s, int k0, int P, const double (&loc)[PPT], double c0, double scale,
+                                double inv_n, const Smem& S) {
+  const int tid = threadIdx.x;
+  int* mark = reinterpret_cast<int*>(S.cum);  // [P] source marks of the outputs
+  const int NT = NW > 0 ? NW * 32 : (int)blockDim.x;
+  const int FS = NT * PPT;
+  const double2* st2 = reinterpret_cast<const double2*>(S.st);
+  const int lane = tid & 31, warp = tid >> 5;
   int hq[PPT];  // count(cum[k]); P = no mark (the last particle, padding)
 #pragma unroll
   for (int q = 0; q < PPT; ++q)
-    hq[q] = k0 + q < P - 1 ? min(P, __double2int_rz(fma(loc[q], (double)P, c0))) : P;
+    hq[q] = k0 + q < P - 1 ? min(P, __double2int_rz(fma(loc[q], scale, c0))) : P;
   // Of a run of consecutive particles with the same count only the last one's
   // mark survives the max, so only it issues the atomic (lane 31's last always
   // does): the same marks with ~P spread atomics instead of P + conflicts.
@@ -923,7 +915,7 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
   int mex = __shfl_sync(0xffffffffu, mi, src);
   const int wtop = __shfl_sync(0xffffffffu, mi, top);
   if (!below) mex = -1;
-  int* wmx = reinterpret_cast<int*>(wsum + 96);
+  int* wmx = reinterpret_cast<int*>(S.red + 2 * kRedSlots + 96);
   st_shared_if(lane == 31, reinterpret_cast<uint32_t*>(wmx) + warp, (uint32_t)wtop);
   ut_bar();
   if constexpr (NW > 0) {
@@ -945,6 +937,44 @@ __device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double in
     }
   }
   // the set buffer is next written by the prefetch after this set's estimate barrier
+}
+
+// pf::resample (tracking.cpp:147-170) on normalised weights: inclusive scan of
+// w in index order (thread, warp, block), then the selection.
+template <int PPT, bool FULL, int NW>
+__device__ void pf_resample(SetRegs<PPT>& s, int k0, int P, double u0, double inv_n, const Smem& S) {
+  const int tid = threadIdx.x;
+  double* wsum = S.red + 2 * kRedSlots;  // [32] warp totals, then [32] int warp maxima at +96
+  resample_stage<PPT, FULL, NW>(s, k0, P, S);
+  double loc[PPT];
+  double run = 0.0;
+#pragma unroll
+  for (int q = 0; q < PPT; ++q) {
+    if (FULL || k0 + q < P) run = q == 0 ? s.w[q] : run + s.w[q];
+    loc[q] = run;
+  }
+  const int lane = tid & 31, warp = tid >> 5;
+  double incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = incl + y;
+  }
+  double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = 0.0;
+  st_shared_if(lane == 31, wsum + warp, incl);
+  resample_zero_marks<PPT, FULL>(k0, P, S);
+  ut_bar();
+  double woff = -0.0;  // cum[k] = (sum of earlier warps' totals + excl) + loc[q]; -0.0: see pf_estimate
+  if constexpr (NW > 0) {
+#pragma unroll
+    for (int v = 0; v < NW - 1; ++v)
+      if (v < warp) woff = woff + wsum[v];
+  } else {
+    for (int v = 0; v < warp; ++v) woff = woff + wsum[v];
+  }
+  const double base = woff + excl;
+  resample_select<PPT, FULL, NW>(s, k0, P, loc, fma(base, (double)P, 1.0 - u0), (double)P, inv_n, S);
 }
 
 // One field of this thread's PPT consecutive particles to / from the set
@@ -1218,7 +1248,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // ---- range updates: own ping, then fused senders (env.cpp:356-360, 385-392)
   SETPROF(2);
   const uint16_t* ml = S.mlist + ti * c.sA;
-  bool have_ess = false;
+  bool have_ess = false, resampled = false;
   double ess = 0.0;
   if (merged) {
     park_field<PPT>(S.park, NT, s.vx);
@@ -1316,39 +1346,80 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         unpark_field<PPT>(S.park + NT * (PPT / 2), NT, s.vy);
       }
     } else {
-      double e[PPT], ls = -0.0, lq = -0.0;  // -0.0: see pf_estimate
+      // e, its running sums (the resample scan's thread part) and squares; the
+      // weight total then comes from the scan's warp totals, so the weight sums
+      // and the resample's scan share one barrier
+      double e[PPT], loc[PPT], run = -0.0, lq = -0.0;  // -0.0: see pf_estimate
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
         e[q] = 0.0;
         if (FULL || k0 + q < P) {
           e[q] = s.w[q] * exp_neg(L[q] - shift, S.tab_exp);
-          ls = ls + e[q];
+          run = run + e[q];
           lq = lq + e[q] * e[q];
         }
+        loc[q] = run;
       }
-      if (merged) {  // before the barrier after which the staging may start
+      if (merged) {
         unpark_field<PPT>(S.park, NT, s.vx);
         unpark_field<PPT>(S.park + NT * (PPT / 2), NT, s.vy);
       }
       SETPROF(4);
+      double incl = run;  // the warp's inclusive scan of the thread totals
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = incl + y;
+      }
+      double excl = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (lane == 0) excl = 0.0;
+      lq = warp_sum(lq);
+      const double* tw = R.buf();  // [0, 32) warp totals of e, [32, 64) of e^2
+      st_shared_if(lane == 31, const_cast<double*>(tw) + warp, incl);
+      st_shared_if(lane == 0, const_cast<double*>(tw) + 32 + warp, lq);
+      // the marks alias the set buffer's w field, which every thread reloaded
+      // before the stage barrier
+      resample_zero_marks<PPT, FULL>(k0, P, S);
+      ut_bar();
+      const double ls = warp_partials_sum<NW>(tw), lsq = warp_partials_sum<NW>(tw + 32);
+      SETPROF(5);
       // the guards on max(e) from the sum: sum >= 2^-850 gives max >= sum / P >=
       // 2^-860 (P <= 1024), sum >= 2^-190 gives max >= 2^-200
-      const double2 r = R.sum2<NW>(ls, lq);
-      SETPROF(5);
-      const bool guard_ok = isfinite(r.x) && r.x >= 0x1p-850;
-      const bool ess_ok = r.x >= 0x1p-190;
+      const bool guard_ok = isfinite(ls) && ls >= 0x1p-850;
+      const bool ess_ok = ls >= 0x1p-190;
       if (guard_ok) {
-        // r.x in [2^-850, P] and r.x^2, r.y >= 2^-400 where the ESS is formed:
+        // ls in [2^-850, P] and ls^2, lsq >= 2^-400 where the ESS is formed:
         // the branch-free IEEE divisions apply
-        const double rcp = div_rn_clamp(1.0, r.x);
-#pragma unroll
-        // (e / sum to ~1 ulp: the merged weights carry the rounding of the tree
-        // sums and of exp anyway; the resample's strata see 1e-16 either way)
-        for (int q = 0; q < PPT; ++q) s.w[q] = e[q] * rcp;
+        const double rcp = div_rn_clamp(1.0, ls);
         // ESS = sum^2 / sum(e^2) unless the squares may have underflowed
         if (ess_ok) {
-          ess = div_rn_clamp(r.x * r.x, r.y);
+          ess = div_rn_clamp(ls * ls, lsq);
           have_ess = true;
+        }
+        if (ess_ok && ess < (double)P / 2.0) {
+          // pf::maybe_resample's resample on the scan above: cum(k) n =
+          // (woff + excl + loc) P / sum, the weights never normalised
+          double woff = -0.0;
+          if constexpr (NW > 0) {
+#pragma unroll
+            for (int v = 0; v < NW - 1; ++v)
+              if (v < warp) woff = woff + tw[v];
+          } else {
+            for (int v = 0; v < warp; ++v) woff = woff + tw[v];
+          }
+          const uint64_t u0_lo = reinterpret_cast<const uint32_t*>(S.bc)[0];
+          const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
+          const double u0 = (double)(((u0_hi << 32) | u0_lo) >> 11) * 0x1.0p-53;
+          const double scale = (double)P * rcp;
+          resample_stage<PPT, FULL, NW>(s, k0, P, S);
+          resample_select<PPT, FULL, NW>(s, k0, P, loc, fma(woff + excl, scale, 1.0 - u0), scale, c.inv_P, S);
+          SETPROF(7);
+          resampled = true;
+        } else {
+#pragma unroll
+          // (e / sum to ~1 ulp: the merged weights carry the rounding of the tree
+          // sums and of exp anyway; the resample's strata see 1e-16 either way)
+          for (int q = 0; q < PPT; ++q) s.w[q] = e[q] * rcp;
         }
       } else {
         exact = true;
@@ -1381,8 +1452,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // so the reference's recomputation cannot resample: skipped unless the state
   // was injected.
   SETPROF(6);
-  bool resampled = false;
-  const bool ess_known_ok = nm == 0 && tk[TK_ESSOK] != 0.0;
+  const bool ess_known_ok = (nm == 0 && tk[TK_ESSOK] != 0.0) || resampled;
   if (!ess_known_ok) {
     if (!have_ess) {
       double w2 = 0.0;
