@@ -1391,12 +1391,16 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         // ls in [2^-850, P] and ls^2, lsq >= 2^-400 where the ESS is formed:
         // the branch-free IEEE divisions apply
         const double rcp = div_rn_clamp(1.0, ls);
-        // ESS = sum^2 / sum(e^2) unless the squares may have underflowed
+        // ESS = sum^2 / sum(e^2) < P / 2 unless the squares may have underflowed,
+        // tested without the division: P / 2 is a power of two, so the product
+        // is exact (the two forms differ only where sum^2 / sum(e^2) rounds up
+        // onto P / 2, ~2^-53 relative)
+        const bool low_ess = ess_ok && ls * ls < ((double)P / 2.0) * lsq;
         if (ess_ok) {
-          ess = div_rn_clamp(ls * ls, lsq);
+          ess = low_ess ? 0.0 : (double)P;  // only its side of P / 2 is used below
           have_ess = true;
         }
-        if (ess_ok && ess < (double)P / 2.0) {
+        if (low_ess) {
           // pf::maybe_resample's resample on the scan above: cum(k) n =
           // (woff + excl + loc) P / sum, the weights never normalised
           double woff = -0.0;
