@@ -45,8 +45,10 @@ def region_table():
         ("set: predict + speed clamp", find("s.px[j] = s.px[j] + s.vx[j] * c.dt;", s0) - 3),
         ("set: likelihood stages", find("// ---- range updates: own ping", s0)),
         ("set: shift + weights + ESS", find("double shift = 0.0;  // sum_j s'_j", s0)),
+        ("set: weight sums + resample scan", find("// e, its running sums (the resample scan's thread part) and squares", s0)),
+        ("set: resample (merged update)", find("// pf::maybe_resample's resample on the scan above", s0)),
         ("set: exact sequential path", find("if (exact && nm > 0) {", s0)),
-        ("set: maybe_resample", find("// ---- pf::maybe_resample", s0)),
+        ("set: maybe_resample (no update / injected state)", find("// ---- pf::maybe_resample", s0)),
         ("set: store to HBM", find("// ---- the set back to HBM", s0)),
         ("set: estimate + track record", find("// ---- estimate (env.cpp:403-407)", s0)),
     ]
@@ -59,6 +61,7 @@ def region_table():
         ("pf_update_seq (exact path)", find("__device__ __noinline__ int pf_update_seq("), None),
         ("pf_estimate", find("__device__ __forceinline__ double3 pf_estimate("), None),
         ("pf_resample", find("__device__ void pf_resample("), None),
+        ("resample_stage / resample_select", find("__device__ __forceinline__ void resample_stage("), None),
         ("stage_env", find("__device__ __forceinline__ void stage_env("), None),
         ("stage_bnd (boundary Philox blocks)", find("void stage_bnd("), None),
         ("prefetch_env", find("void prefetch_env("), None),
