@@ -774,7 +774,8 @@ __device__ __noinline__ int pf_update_seq(const double* m, int k0, int P, const 
 // pf::estimate (tracking.cpp:180-188) in ONE reduction: moments about the set's
 // previous estimate (cx, cy), mean = c + sum w (p - c), spread^2 = second moment
 // minus the squared shift; exact second pass when that subtraction could lose
-// more than ~1e-11 relative.
+// more than ~1e-11 relative. Returns (mean x, mean y, spread^2): the caller takes
+// the square root in the one thread that writes the record.
 template <int PPT, bool FULL, int NW>
 __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, int P, double cx, double cy,
                                                BlockReducer& R, bool uniform = false, double inv_n = 0.0) {
@@ -809,7 +810,7 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
   const double shift2 = m.x * m.x + m.y * m.y;
   const double var = m.z - shift2;
   // var > 0 here; far above 2^-960 for any spread a set can have
-  if (var > 1e-5 * shift2) return make_double3(mx, my, sqrt_rn_clamp(var));
+  if (var > 1e-5 * shift2) return make_double3(mx, my, var);
   double acc = 0.0;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
@@ -818,7 +819,7 @@ __device__ __forceinline__ double3 pf_estimate(const SetRegs<PPT>& s, int k0, in
       acc = acc + s.w[j] * (dx * dx + dy * dy);
     }
   }
-  return make_double3(mx, my, sqrt_rn_clamp(R.sum<NW>(acc)));  // >= 0: 0 or far above 2^-960
+  return make_double3(mx, my, R.sum<NW>(acc));  // >= 0: 0 or far above 2^-960
 }
 
 // Stage this thread's particles for the resample gather: particle k = k0 + q of
@@ -1520,7 +1521,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     const Rec rec = rec_of(B, e);
     TRK(K_EX, ti) = est.x;
     TRK(K_EY, ti) = est.y;
-    TRK(K_SPREAD, ti) = est.z;
+    TRK(K_SPREAD, ti) = sqrt_rn_clamp(est.z);  // the spread^2 -> spread in the one thread writing it
     TRK(K_AGE, ti) = fresh ? 0.0 : tk[TK_AGE] + 1.0;
     TRK(K_EVER, ti) = (tk[TK_EVER] != 0.0 || fresh) ? 1.0 : 0.0;
     // stream position: 4P predict draws, 2 for a resample (tracking.cpp:24-37, 160)
@@ -1741,7 +1742,7 @@ __device__ void reinit_set(const DevConfig& c, const DevBatch& B, const Smem& S,
   if (tid == 0) {
     TRK(K_EX, ti) = est.x;
     TRK(K_EY, ti) = est.y;
-    TRK(K_SPREAD, ti) = est.z;
+    TRK(K_SPREAD, ti) = sqrt_rn_clamp(est.z);  // the spread^2 -> spread in the one thread writing it
     TRK(K_AGE, ti) = 0.0;
     TRK(K_EVER, ti) = 0.0;
     TRK(K_POS, ti) = (double)(pos + 8ull * (uint64_t)P);
