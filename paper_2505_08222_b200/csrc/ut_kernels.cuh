@@ -919,7 +919,16 @@ __device__ void resample_select(SetRegs<PPT>& s, int k0, int P, const double (&l
   int* wmx = reinterpret_cast<int*>(S.red + 2 * kRedSlots + 96);
   st_shared_if(lane == 31, reinterpret_cast<uint32_t*>(wmx) + warp, (uint32_t)wtop);
   ut_bar();
-  if constexpr (NW > 0) {
+  if constexpr (NW > 0 && NW % 4 == 0) {  // the warp maxima as int4 loads
+#pragma unroll
+    for (int v = 0; v < NW; v += 4) {
+      const int4 m4 = *reinterpret_cast<const int4*>(wmx + v);
+      if (v < warp) mex = max(mex, m4.x);
+      if (v + 1 < warp) mex = max(mex, m4.y);
+      if (v + 2 < warp) mex = max(mex, m4.z);
+      if (v + 3 < warp) mex = max(mex, m4.w);
+    }
+  } else if constexpr (NW > 0) {
 #pragma unroll
     for (int v = 0; v < NW - 1; ++v)
       if (v < warp) mex = max(mex, wmx[v]);
@@ -1382,7 +1391,29 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       // before the stage barrier
       resample_zero_marks<PPT, FULL>(k0, P, S);
       ut_bar();
-      const double ls = warp_partials_sum<NW>(tw), lsq = warp_partials_sum<NW>(tw + 32);
+      // the warp totals once in registers: the block total (warp_partials_sum's
+      // tree) and, for a resample, the earlier warps' share come from the same loads
+      constexpr int NWT = NW >= 2 && (NW & (NW - 1)) == 0 ? NW : 1;
+      double tv[NWT];
+      double ls;
+      if constexpr (NWT > 1) {
+#pragma unroll
+        for (int i = 0; i < NWT; i += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(tw + i);
+          tv[i] = t2.x, tv[i + 1] = t2.y;
+        }
+        double v[NWT];
+#pragma unroll
+        for (int i = 0; i < NWT; ++i) v[i] = tv[i];
+#pragma unroll
+        for (int st = 1; st < NWT; st *= 2)
+#pragma unroll
+          for (int i = 0; i < NWT; i += 2 * st) v[i] = v[i] + v[i + st];
+        ls = v[0];
+      } else {
+        ls = warp_partials_sum<NW>(tw);
+      }
+      const double lsq = warp_partials_sum<NW>(tw + 32);
       SETPROF(5);
       // the guards on max(e) from the sum: sum >= 2^-850 gives max >= sum / P >=
       // 2^-860 (P <= 1024), sum >= 2^-190 gives max >= 2^-200
@@ -1405,10 +1436,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           // pf::maybe_resample's resample on the scan above: cum(k) n =
           // (woff + excl + loc) P / sum, the weights never normalised
           double woff = -0.0;
-          if constexpr (NW > 0) {
+          if constexpr (NWT > 1) {
 #pragma unroll
-            for (int v = 0; v < NW - 1; ++v)
-              if (v < warp) woff = woff + tw[v];
+            for (int v = 0; v < NWT - 1; ++v)
+              if (v < warp) woff = woff + tv[v];
           } else {
             for (int v = 0; v < warp; ++v) woff = woff + tw[v];
           }
