@@ -1235,13 +1235,18 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // skip the correctly rounded sqrt and division (about half of them: the fast
   // particles cluster after resampling). Otherwise branch-free per particle (sp
   // = 0 gives a quotient the select drops).
+  // The test runs on the high words (for doubles >= 0 their order is the integer
+  // order, and hi(v2) < hi(lo) implies v2 < lo; ties and NaN only send a warp
+  // to the exact branch): integer compares, where an "any v2 > lo" over doubles
+  // compiles to an fp64 max reduction with NaN fix-ups.
   const double lo = (ms * ms) * (1.0 - 0x1p-50);
+  const int lo_hi = __double2hiint(lo);
   double v2[PPT];
   bool over = false;
 #pragma unroll
   for (int j = 0; j < PPT; ++j) {
     v2[j] = s.vx[j] * s.vx[j] + s.vy[j] * s.vy[j];
-    over |= v2[j] > lo;
+    over |= __double2hiint(v2[j]) >= lo_hi;
   }
   if (ms > 0.0 && __any_sync(0xffffffffu, over)) {
 #pragma unroll
