@@ -889,10 +889,17 @@ __device__ void resample_select(SetRegs<PPT>& s, int k0, int P, const double (&l
   // does): the same marks with ~P spread atomics instead of P + conflicts.
   int nxt = __shfl_down_sync(0xffffffffu, hq[0], 1);
   if (lane == 31) nxt = -1;
+  // Unconditional: a lane without a mark adds max(., 0) -- a no-op, marks are
+  // >= 0 -- at its own lane-contiguous slot (no bank conflicts), so the warp
+  // issues the reduction without a branch around it (ptxas does not predicate
+  // ATOMS: a predicated red.shared becomes BSSY / BRA / BSYNC).
+  const int NTm = NW > 0 ? NW * 32 : (int)blockDim.x;
 #pragma unroll
   for (int q = 0; q < PPT; ++q) {
     const int hn = q + 1 < PPT ? hq[q + 1] : nxt;
-    red_max_shared_if(hq[q] < P && hq[q] != hn, mark + min(hq[q], P - 1), k0 + q + 1);
+    const bool p = hq[q] < P && hq[q] != hn;
+    int* adr = p ? mark + min(hq[q], P - 1) : mark + ((q * NTm + tid) & (P - 1));
+    atomicMax(adr, p ? k0 + q + 1 : 0);
   }
   ut_bar();
   int r[PPT];
