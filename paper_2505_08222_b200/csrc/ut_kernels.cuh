@@ -1143,8 +1143,40 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   float zpx[PPT], zpy[PPT], zvx[PPT], zvy[PPT];  // out[k], out[P+k], out[2P+k], out[3P+k]
   if (noise) {
     uint32_t W[4][PPT];  // [segment][particle]
-    if (FULL) {
+    if (FULL && (off == 0 || off == 2)) {
+      // The stream positions of the particle sets stay even (4P per predict, 2
+      // per resample, 8P at init), so the window starts at word 0 or 2 of the
+      // thread's first block (block-uniform): no shuffles and no selects at 0,
+      // two shuffles and a compile-time shift at 2.
       static_assert(PPT % 4 == 0, "the FULL path takes whole Philox blocks");
+      if (off == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            W[q][4 * i] = blk[q][i].x, W[q][4 * i + 1] = blk[q][i].y;
+            W[q][4 * i + 2] = blk[q][i].z, W[q][4 * i + 3] = blk[q][i].w;
+          }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t nx = __shfl_down_sync(0xffffffffu, blk[q][0].x, 1);
+          uint32_t ny = __shfl_down_sync(0xffffffffu, blk[q][0].y, 1);
+          if (lane == 31) {  // the block after the warp's range (stage_bnd)
+            const uint4 xq = bnd[q * nw + warp];
+            nx = xq.x, ny = xq.y;
+          }
+          uint32_t a[4 * NB + 2];
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            a[4 * i] = blk[q][i].x, a[4 * i + 1] = blk[q][i].y, a[4 * i + 2] = blk[q][i].z, a[4 * i + 3] = blk[q][i].w;
+          }
+          a[4 * NB] = nx, a[4 * NB + 1] = ny;
+#pragma unroll
+          for (int j = 0; j < PPT; ++j) W[q][j] = a[j + 2];
+        }
+      }
+    } else if (FULL) {  // any other start word (an injected state): the general window
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         // this thread's window: its NB blocks, then the next lane's first block
