@@ -1323,19 +1323,22 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     // conservative), so the stage maxima are taken from the high words only.
     double L[PPT];
 #pragma unroll
-    for (int q = 0; q < PPT; ++q) L[q] = 0.0;
+    for (int q = 0; q < PPT; ++q) L[q] = -0.0;  // sum_j tq_j^2 (-0.0: see pf_estimate)
     // per-stage warp maxima, [stage * kMbStride + warp]: the stride keeps the
     // stage lanes' 128-bit reads below on distinct banks
     float* mb = reinterpret_cast<float*>(R.buf());
-    // one stage: every particle's log-likelihood for measurement j, added to L in
-    // stage order, and the stage's warp maximum (rounded up to fp32)
-    // Every ll is <= 0, so its high word, read as unsigned, grows with |ll|: the
-    // smallest high word is that of the largest ll, and as a double with a zero
-    // low word it is an upper bound of it (the mantissa is truncated toward 0).
-    // One unsigned min per particle and one REDUX per stage give s'_j.
+    // Every measurement of the env has the same noise (c2 = -1/(2 sigma^2), one
+    // config per env), so sum_j ll_ij = c2 sum_j tq_ij^2 with tq = d - r: one fma
+    // per particle and stage, the product by c2 (and the shift) folded into the
+    // exp's argument later -- the same log-likelihood to a few ulp.
+    // The stage maximum s_j = c2 min_i tq_ij^2 comes from the smallest |tq|:
+    // its high word (sign cleared; doubles >= 0 order like their bits) read back
+    // with a zero low word is a lower bound lb_j of min |tq|, so c2 lb_j^2 is an
+    // upper bound s'_j of s_j. One unsigned min per particle, one REDUX per stage.
+    const double c2 = S.meas[kMeasStride * ml[0] + 4];
     auto stage = [&](int j) -> uint32_t {
       const double* m = S.meas + kMeasStride * ml[j];
-      const double ox = m[0], oy = m[1], r2 = m[2], c2 = m[4];
+      const double ox = m[0], oy = m[1], r2 = m[2];
       uint32_t mj = 0xFFFFFFFFu;
 #pragma unroll
       for (int q = 0; q < PPT; ++q) {
@@ -1343,9 +1346,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           const double dx = s.px[q] - ox, dy = s.py[q] - oy;
           const double d = sqrt_dist(fma(dx, dx, dy * dy));
           const double tq = d - r2;
-          const double ll = (tq * tq) * c2;  // -(1/2)((d - r)/sigma)^2 to a few ulp
-          L[q] = L[q] + ll;
-          mj = min(mj, (uint32_t)__double2hiint(ll));
+          L[q] = fma(tq, tq, L[q]);
+          mj = min(mj, (uint32_t)__double2hiint(tq) & 0x7FFFFFFFu);
         }
       }
       return mj;
@@ -1387,7 +1389,8 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
     // lane of the group ends with the same operands in the same pairing), then
     // lane 0's total to the warp
     {
-      double sj = lane < nm ? __hiloint2double((int)hl, 0) : 0.0;  // >= max_i ll_ij
+      const double lb = __hiloint2double((int)hl, 0);
+      double sj = lane < nm ? c2 * (lb * lb) : 0.0;  // >= max_i ll_ij
       sj = sj + __shfl_xor_sync(0xffffffffu, sj, 4);
       sj = sj + __shfl_xor_sync(0xffffffffu, sj, 2);
       sj = sj + __shfl_xor_sync(0xffffffffu, sj, 1);
@@ -1408,7 +1411,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       for (int q = 0; q < PPT; ++q) {
         e[q] = 0.0;
         if (FULL || k0 + q < P) {
-          e[q] = s.w[q] * exp_neg(L[q] - shift, S.tab_exp);
+          e[q] = s.w[q] * exp_neg(fma(L[q], c2, -shift), S.tab_exp);  // L = sum tq^2 here
           run = run + e[q];
           lq = lq + e[q] * e[q];
         }
