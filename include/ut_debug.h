@@ -17,7 +17,8 @@ int ut_debug_cr_grid(int kind, int device, float* host_out);
  * (kind 1) for the particle speed clamp that differ from IEEE __dsqrt_rn /
  * __ddiv_rn over n random operands of the clamp's domain; kind 2 / 3: the
  * likelihood distance sqrt (sqrt_dist) results more than 1 ulp / any ulp away
- * from IEEE over squared distances in [0, 2^31]; kind 4: the particle-weight exp
+ * from IEEE over squared distances in [2^-60, 2^31] (x = 0 gives NaN by design: the
+ * step then takes its exact path); kind 4: the particle-weight exp
  * (exp_neg) results more than 1 ulp away from libm exp over [-760, 0]. */
 int ut_debug_ieee_check(int kind, uint64_t seed, int64_t n, int device, uint64_t* mismatches);
 /* n consecutive Philox4x32-10 blocks from block0 (rng.hpp:116-131): 4n words. */

