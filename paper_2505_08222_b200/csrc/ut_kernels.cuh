@@ -1428,8 +1428,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
         const double y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl = incl + y;
       }
-      double excl = __shfl_up_sync(0xffffffffu, incl, 1);
-      if (lane == 0) excl = 0.0;
+      // the thread's exclusive prefix as incl - run (no shuffle; it differs from
+      // the previous lane's incl by rounding only, which the resample's marks
+      // tolerate: counts only need to be consistent within a thread)
+      const double excl = incl - run;
       lq = warp_sum(lq);
       const double* tw = R.buf();  // [0, 32) warp totals of e, [32, 64) of e^2
       st_shared_if(lane == 31, const_cast<double*>(tw) + warp, incl);
