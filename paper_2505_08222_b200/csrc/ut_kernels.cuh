@@ -1302,7 +1302,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   // ---- range updates: own ping, then fused senders (env.cpp:356-360, 385-392)
   SETPROF(2);
   const uint16_t* ml = S.mlist + ti * c.sA;
-  bool have_ess = false, resampled = false;
+  bool have_ess = false, resampled = false, w_early = false;
   double ess = 0.0;
   if (merged) {
     park_field<PPT>(S.park, NT, s.vx);
@@ -1496,6 +1496,12 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
           const uint64_t u0_hi = reinterpret_cast<const uint32_t*>(S.bc)[1];
           const double u0 = (double)(((u0_hi << 32) | u0_lo) >> 11) * 0x1.0p-53;
           const double scale = (double)P * rcp;
+          if (FULL) {  // the resampled weights are all 1/n: stored now, draining under the gather
+            const size_t wb = (size_t)gset * P;
+#pragma unroll
+            for (int q = 0; q < PPT; q += 4) st_global_v4(B.w + wb + k0 + q, c.inv_P, c.inv_P, c.inv_P, c.inv_P);
+            w_early = true;
+          }
           resample_stage<PPT, FULL, NW>(s, k0, P, S);
           resample_select<PPT, FULL, NW>(s, k0, P, loc, fma(woff + excl, scale, 1.0 - u0), scale, c.inv_P, S);
           SETPROF(7);
@@ -1571,7 +1577,10 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       // first, are the ones the estimate's temporaries get
       st_global_v4(B.vx + base + k0 + q, s.vx[q], s.vx[q + 1], s.vx[q + 2], s.vx[q + 3]);
       st_global_v4(B.vy + base + k0 + q, s.vy[q], s.vy[q + 1], s.vy[q + 2], s.vy[q + 3]);
-      st_global_v4(B.w + base + k0 + q, s.w[q], s.w[q + 1], s.w[q + 2], s.w[q + 3]);
+      // w: stored at the resample decision (w_early), or unchanged since the
+      // load (no update and no resample this step)
+      if (!w_early && !(nm == 0 && tk[TK_ESSOK] != 0.0))
+        st_global_v4(B.w + base + k0 + q, s.w[q], s.w[q + 1], s.w[q + 2], s.w[q + 3]);
       st_global_v4(B.px + base + k0 + q, s.px[q], s.px[q + 1], s.px[q + 2], s.px[q + 3]);
       st_global_v4(B.py + base + k0 + q, s.py[q], s.py[q + 1], s.py[q + 2], s.py[q + 3]);
     }
