@@ -1581,8 +1581,7 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
       // load (no update and no resample this step)
       if (!w_early && !(nm == 0 && tk[TK_ESSOK] != 0.0))
         st_global_v4(B.w + base + k0 + q, s.w[q], s.w[q + 1], s.w[q + 2], s.w[q + 3]);
-      st_global_v4(B.px + base + k0 + q, s.px[q], s.px[q + 1], s.px[q + 2], s.px[q + 3]);
-      st_global_v4(B.py + base + k0 + q, s.py[q], s.py[q + 1], s.py[q + 2], s.py[q + 3]);
+      // px, py: after the estimate, which reads them (see there)
     }
   } else {
 #pragma unroll
@@ -1604,6 +1603,16 @@ __device__ void step_set(const DevConfig& c, const DevBatch& B, const Smem& S, B
   if (FULL) fence_proxy_async();
   SETPROF(8);
   const double3 est = pf_estimate<PPT, FULL, NW>(s, k0, P, tk[TK_EX], tk[TK_EY], R, resampled, c.inv_P);
+  // the positions stored only now: they stay live for the estimate anyway, and
+  // the estimate's temporaries no longer wait (WAR, long scoreboard) for 256-bit
+  // stores still reading the registers they are given
+  if (FULL) {
+#pragma unroll
+    for (int q = 0; q < PPT; q += 4) {
+      st_global_v4(B.px + base + k0 + q, s.px[q], s.px[q + 1], s.px[q + 2], s.px[q + 3]);
+      st_global_v4(B.py + base + k0 + q, s.py[q], s.py[q + 1], s.py[q + 2], s.py[q + 3]);
+    }
+  }
   SETPROF(9);
   if (FULL && tid == 0 && next >= 0) prefetch_set(B, S, next, P);
   if (tid == 0) {
